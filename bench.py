@@ -1,0 +1,457 @@
+#!/usr/bin/env python
+"""Benchmark: full Pauli decomposition of a dense 2^N x 2^N complex128 matrix on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--qubits 14]
+
+A step is one full decomposition (all 4^N coefficients) of the N=14 matrix of BASELINE.json
+configs[4] (the reference's seeded uniform[-1,1) generator, 4 GiB), on the Gray-code path:
+K1 diagonal gather + K2 Gray-code FP64 sums (+ NCCL broadcast of G and gather of the
+coefficient runs when N > 1, one process per GPU under torchrun). Rank 0 prints one JSON line.
+
+--impl reference times the reference's own CPU implementation (oracle/_ref/libpdref.so: the
+reference's proj/src compiled unmodified, coeff_fast over all host threads) on a seeded
+sample of X-masks of the same workload, scaled per coefficient.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+ACCEPT_SEED = 20260823  # proj/tests/acceptance.cpp:30
+METRIC = "pauli_coeffs_per_sec"
+UNIT = "coeff/s"
+SM_COUNT = 148
+FP64_LANES_PER_SM = 64
+
+
+def parse_args():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--qubits", type=int, default=14)
+    ap.add_argument("--path", choices=["gray", "wht"], default="gray")
+    ap.add_argument("--sample-masks", type=int, default=8, help="X-masks in the CPU sample (>= 8)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the N=12 and WHT side lines")
+    return ap.parse_args()
+
+
+def workload_config(nq: int, world: int, path: str) -> dict:
+    return {
+        "workload": f"full decomposition N={nq} (BASELINE configs[4])" if nq == 14
+        else f"full decomposition N={nq}",
+        "num_qubits": nq,
+        "coefficients": 4**nq,
+        "matrix": f"random_matrix({nq}, matrix_seed({ACCEPT_SEED},{nq},0)): uniform[-1,1) complex128, "
+                  f"{16 * 4**nq / 2**30:g} GiB (reference generator, bit-exact on device)",
+        "path": "gray-code K1+K2" if path == "gray" else "walsh-hadamard K1+K4",
+        "parallelism": f"xmask-shard x{world}" + (" (NCCL broadcast G + grouped send/recv gather)" if world > 1 else ""),
+        "l2": "inputs (4 GiB G, 4 GiB diagonals) exceed the 126 MB L2; no flush needed" if nq >= 12
+        else "inputs smaller than L2",
+    }
+
+
+# ---------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, local_rank: int):
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        self.index = vis.split(",")[local_rank] if vis else str(local_rank)
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", self.index], stdout=self.fh, stderr=subprocess.DEVNULL)
+        except (OSError, ValueError):
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.fh.close()
+        sm, smax, power, reasons = [], [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+                power.append(float(parts[3]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "power_w_max": max(power) if power else None,
+                "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+# ---------------------------------------------------------------- reference arm
+
+def cpu_sample_masks(nq: int, k: int) -> list:
+    import numpy as np
+    rng = np.random.default_rng(ACCEPT_SEED + nq)
+    return sorted(int(x) for x in rng.choice(2**nq, size=min(k, 2**nq), replace=False))
+
+
+class CpuBaseline:
+    """The reference's CPU path on this host: coeff_fast on every string of k seeded X-masks
+    (ascending n, contiguous split over all hardware threads), BASELINE.md §2."""
+
+    def __init__(self, nq: int, k: int, host_matrix=None):
+        import numpy as np
+        from oracle import oracle as O
+        self.nq = nq
+        self.ref = O.reference()
+        self.kind = "reference" if self.ref is not None else "port"
+        self.masks = cpu_sample_masks(nq, k)
+        self.ns = O.xmask_sample_indices(nq, self.masks)
+        seed = O.port().matrix_seed(ACCEPT_SEED, nq, 0)
+        if self.ref is not None:
+            self.cores = self.ref.cores
+            self.h = self.ref.matrix(host_matrix) if host_matrix is not None else \
+                self.ref.random_matrix_handle(nq, seed)
+        else:
+            self.cores = os.cpu_count() or 1
+            self.port = O.port()
+            self.g = host_matrix if host_matrix is not None else self.port.random_matrix(nq, seed)
+        self.sample = (f"{len(self.masks)} seeded X-masks x all {2**nq} Z-masks = {self.ns.size} "
+                       f"coefficients of the N={nq} workload via "
+                       + ("reference coeff_fast (proj/src, -O3)" if self.kind == "reference"
+                          else "oracle port of coeff_fast")
+                       + f" on {self.cores} threads; throughput scales linearly to all 4^N")
+
+    def run_once(self) -> float:
+        t0 = time.perf_counter()
+        if self.kind == "reference":
+            self.out = self.ref.coeff_batch(self.h, self.ns, threads=self.cores)
+        else:
+            self.out = self.port.coeff_batch(self.g, self.ns, threads=self.cores)
+        return time.perf_counter() - t0
+
+
+def run_reference_arm(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return  # only rank 0 times the CPU reference; other ranks exit without work
+    nq = args.qubits
+    base = CpuBaseline(nq, max(8, args.sample_masks))
+    for _ in range(args.warmup):
+        base.run_once()
+    times = [base.run_once() for _ in range(args.steps)]
+    per_step = sum(times) / len(times)
+    value = base.ns.size / per_step
+    line = {
+        "impl": "reference",
+        "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": per_step * 1e3,
+        "ms_per_full_decomposition_est": 4**nq / value * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": workload_config(nq, args.gpus, "gray"),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": base.cores, "kind": base.kind,
+                         "sample": base.sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- our arm
+
+def run_ours(args) -> None:
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2401_16378_b200 as pd
+    from paper_2401_16378_b200.sharding import ShardPlan
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    nq = args.qubits
+    dim = 1 << nq
+    plan = ShardPlan(nq, world, rank)
+    stream = torch.cuda.current_stream(dev)
+    sptr = stream.cuda_stream
+    pd.set_device(local_rank)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local_rank])
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    G = torch.empty((dim, dim), dtype=torch.complex128, device=dev)
+    from oracle import oracle as O  # generator seed only (bench setup, outside the timed path)
+    pd_seed = O.port().matrix_seed(ACCEPT_SEED, nq, 0)
+    if rank == 0:
+        pd.device.random_matrix(nq, pd_seed, G.data_ptr(), sptr)
+    diag = torch.empty(plan.x_count * dim, dtype=torch.complex128, device=dev)
+    out = torch.empty(4**nq, dtype=torch.complex128, device=dev) if rank == 0 else None
+    local = None if rank == 0 else torch.empty(plan.run_len << plan.run_bits,
+                                               dtype=torch.complex128, device=dev)
+    if rank == 0:
+        runs = [out[o:o + plan.run_len] for o in plan.offsets()]
+    else:
+        runs = [local[r * plan.run_len:(r + 1) * plan.run_len] for r in range(1 << plan.run_bits)]
+    run_ptrs = [r.data_ptr() for r in runs]
+
+    def gather():
+        if world == 1:
+            return
+        ops = []
+        if rank == 0:
+            for src in range(1, world):
+                for o in plan.offsets(src):
+                    ops.append(dist.P2POp(dist.irecv, out[o:o + plan.run_len], src))
+        else:
+            for r in runs:
+                ops.append(dist.P2POp(dist.isend, r, 0))
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+
+    def step(path, ev=None):
+        if world > 1:
+            dist.broadcast(G, src=0)
+        if ev is not None:
+            ev[0].record(stream)
+        pd.device.diag_gather(nq, G.data_ptr(), plan.x0, plan.x_count, diag.data_ptr(), sptr)
+        if ev is not None:
+            ev[1].record(stream)
+        pd.device.xmask_coeffs(nq, diag.data_ptr(), plan.x0, plan.x_count, plan.run_bits,
+                               run_ptrs, path, sptr)
+        if ev is not None:
+            ev[2].record(stream)
+        gather()
+
+    def timed(path, steps, warmup, sample_clocks=False):
+        for _ in range(warmup):
+            step(path)
+        torch.cuda.synchronize()
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        clocks = ClockSampler(local_rank) if sample_clocks else None
+        if clocks:
+            clocks.start()
+        barrier()
+        torch.cuda.synchronize()
+        l0 = pd.launch_count()
+        t0.record(stream)
+        for s in range(steps):
+            step(path, evs[s])
+        t1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        launches = pd.launch_count() - l0
+        ck = clocks.stop() if clocks else None
+        ms = max_over_ranks(t0.elapsed_time(t1))
+        k1 = sum(e[0].elapsed_time(e[1]) for e in evs) / steps
+        k2 = sum(e[1].elapsed_time(e[2]) for e in evs) / steps
+        return ms, k1, k2, launches, ck
+
+    # FP64-add probe (peak context) and the headline measurement
+    probe = pd.fp64_add_probe(local_rank)
+    ms, k1_ms, k2_ms, launches, clocks = timed(args.path, args.steps, args.warmup, sample_clocks=True)
+    per_step_ms = ms / args.steps
+    value = 4**nq / (per_step_ms / 1e3)
+
+    # roofline of the dominant kernel (K2 Gray: FP64-add bound; K4 WHT: HBM bound)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        pass
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        traffic = prof.get(f"N{nq}_{args.path}_x{world}")
+    except (OSError, ValueError):
+        pass
+    if args.path == "gray":
+        dadd = 2.0 * dim * (4**nq / world)  # 2 DADD per term, 2^N terms per coefficient
+        achieved = dadd / (k2_ms / 1e3) / 1e12
+        peak = SM_COUNT * FP64_LANES_PER_SM * sm_max * 1e6 / 1e12
+        roofline = {"bound": "fp64", "kernel": "gray_xmask_kernel (K2)", "achieved": achieved,
+                    "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                    "algorithmic": f"2*2^N DADD per coefficient = {dadd:.4g} DADD per launch",
+                    "peak_source": f"nominal FP64 add: {SM_COUNT} SM x {FP64_LANES_PER_SM} lanes x "
+                                   f"{sm_max:g} MHz (MEASURED_PEAKS.json has no FP64 entry)",
+                    "probe_tflops": probe / 1e12, "frac_of_probe": achieved / (probe / 1e12),
+                    "k1_gather_ms": k1_ms, "k2_ms": k2_ms,
+                    "k1_gather_gbs": 32.0 * 4**nq / world / (k1_ms / 1e3) / 1e9}
+    else:
+        byts = 32.0 * 4**nq / world
+        achieved = byts / ((k1_ms + k2_ms) / 1e3) / 1e9
+        peak = float(peaks.get("hbm_gbs", 6542.7))
+        roofline = {"bound": "hbm", "kernel": "K1 gather + K4 WHT", "achieved": achieved,
+                    "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": per_step_ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": workload_config(nq, world, args.path),
+        "roofline": roofline,
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+
+    # ---- cpu_baseline: the reference on this host, rank 0 at N=1 only
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        gh = G.cpu().numpy()
+        base = CpuBaseline(nq, max(8, args.sample_masks), host_matrix=gh)
+        secs = base.run_once()
+        # the device result must match the reference on the sampled strings, value for value
+        got = out[torch.from_numpy(base.ns.astype(np.int64)).to(dev)].cpu().numpy() \
+            if args.path == "gray" else None
+        line["cpu_baseline"] = {"value": base.ns.size / secs, "unit": UNIT, "cores": base.cores,
+                                "kind": base.kind, "sample": base.sample,
+                                "seconds": secs}
+        if got is not None:
+            line["cpu_baseline"]["sample_matches_gpu"] = bool(np.all(got == base.out))
+        del gh, base
+
+    # ---- side measurements: N=12 (the metric's other size) and the WHT path
+    if not args.no_extras:
+        if args.path == "gray":
+            ms_w, k1w, k4w, _, _ = timed("wht", args.steps, max(3, args.warmup))
+            byts = 32.0 * 4**nq / world
+            line["wht_path"] = {"value": 4**nq / (ms_w / args.steps / 1e3), "unit": UNIT,
+                                "ms_per_step": ms_w / args.steps,
+                                "roofline": {"bound": "hbm", "achieved": byts / ((k1w + k4w) / 1e3) / 1e9,
+                                             "peak": float(peaks.get("hbm_gbs", 6542.7)), "unit": "GB/s",
+                                             "algorithmic": "32*4^N B (read G once, write coefficients once)",
+                                             "k1_ms": k1w, "k4_ms": k4w}}
+            line["wht_path"]["roofline"]["frac"] = (line["wht_path"]["roofline"]["achieved"]
+                                                    / line["wht_path"]["roofline"]["peak"])
+
+    # ---- e2e through the public API with pinned host buffers (H2D + D2H inside)
+    if not args.no_e2e:
+        del diag, local
+        e2e = run_e2e(args, pd, plan, G, out, dev, stream, barrier, max_over_ranks, world, rank)
+        line["e2e"] = e2e
+
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, pd, plan, G, out, dev, stream, barrier, max_over_ranks, world, rank):
+    """The user-facing call on host memory. N=1: paper_2401_16378_b200.decompose(G_host, out=...)
+    (C ABI pd_decompose: H2D, K1, K2, D2H). N>1: rank 0 uploads G, ShardedDecomposer runs the
+    broadcast/compute/gather, rank 0 downloads the coefficients."""
+    import torch
+
+    nq = args.qubits
+    nbytes = 16 * 4**nq
+    steps = max(1, min(args.steps, 5))
+    if world == 1:
+        gh_t = torch.empty(G.shape, dtype=torch.complex128, pin_memory=True)
+        gh_t.copy_(G)
+        oh_t = torch.empty(4**nq, dtype=torch.complex128, pin_memory=True)
+        gh, oh = gh_t.numpy(), oh_t.numpy()
+        pd.decompose(gh, out=oh, path=args.path)  # warm-up: the context allocates its buffers
+        times = []
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            pd.decompose(gh, out=oh, path=args.path)
+            times.append(time.perf_counter() - t0)
+        per = sum(times) / len(times)
+        return {"value": 4**nq / per, "unit": UNIT, "h2d_bytes_per_step": nbytes,
+                "d2h_bytes_per_step": nbytes, "ms_per_step": per * 1e3,
+                "api": "paper_2401_16378_b200.decompose(pinned numpy, out=pinned numpy)"}
+    from paper_2401_16378_b200.sharding import ShardedDecomposer
+    sd = ShardedDecomposer(nq, dev, path=args.path)
+    gh_t = oh_t = None
+    if rank == 0:
+        gh_t = torch.empty(G.shape, dtype=torch.complex128, pin_memory=True)
+        gh_t.copy_(G)
+        oh_t = torch.empty(4**nq, dtype=torch.complex128, pin_memory=True)
+
+    def one():
+        if rank == 0:
+            G.copy_(gh_t, non_blocking=True)
+        sd(G, out)
+        if rank == 0:
+            oh_t.copy_(out, non_blocking=True)
+        torch.cuda.synchronize()
+
+    one()
+    barrier()
+    times = []
+    for _ in range(steps):
+        barrier()
+        t0 = time.perf_counter()
+        one()
+        barrier()
+        times.append(time.perf_counter() - t0)
+    per = max_over_ranks(sum(times) / len(times))
+    return {"value": 4**nq / per, "unit": UNIT,
+            "h2d_bytes_per_step": nbytes if rank == 0 else 0,
+            "d2h_bytes_per_step": nbytes if rank == 0 else 0, "ms_per_step": per * 1e3,
+            "api": "paper_2401_16378_b200.sharding.ShardedDecomposer with pinned host G/out on rank 0"}
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,152 @@
+/*
+ * pd_api.h — C ABI of the B200 Pauli-decomposition library (libpd_b200.so).
+ *
+ * This is the drop-in boundary for the reference's hot path. The reference
+ * (arXiv 2401.16378, proj/) has no FFI of its own: its boundary is the C++
+ * declarations in proj/include/paulidecomp/decompose.hpp:33-56 and
+ * matrix.hpp:14-51, exposed to Python by proj/bindings/module.cpp:56-121.
+ * Each entry point below names the reference interface it replaces.
+ *
+ * Conventions (all functions):
+ *   - plain pointers and sizes; no C++ or CUDA types. Matrices are row-major
+ *     dim x dim complex128 stored as interleaved (re, im) doubles — the layout
+ *     of std::complex<double> / numpy complex128 — so element (row j, col i)
+ *     is at doubles [2*(j*dim+i), 2*(j*dim+i)+1] (matrix.hpp:10-13).
+ *   - coefficient arrays are indexed by tensor number n: base-4 digit t of n
+ *     selects sigma_t in {I,X,Y,Z}, digit 0 rightmost (pauli.hpp:13-20).
+ *   - return value is a pd_status; on failure pd_last_error() holds the message
+ *     (thread-local). PD_EINVAL / PD_ELENGTH mirror std::invalid_argument /
+ *     std::length_error thrown by the reference (decompose.cpp:14-19,98-99;
+ *     matrix.cpp:10-19).
+ *   - *_device functions take device pointers and a cudaStream_t passed as
+ *     void* (NULL = legacy default stream) and are stream-ordered; host-buffer
+ *     functions are synchronous, like the reference's calls.
+ *   - there is no CPU fallback: without a usable sm_100 GPU every compute
+ *     entry point returns PD_ENODEV.
+ */
+#ifndef PD_API_H
+#define PD_API_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PD_API_VERSION 1
+
+#if defined(__GNUC__)
+#define PD_EXPORT __attribute__((visibility("default")))
+#else
+#define PD_EXPORT
+#endif
+
+typedef enum pd_status {
+    PD_OK = 0,
+    PD_EINVAL = -1,  /* std::invalid_argument in the reference */
+    PD_ELENGTH = -2, /* std::length_error */
+    PD_ENOMEM = -3,  /* std::bad_alloc / cudaErrorMemoryAllocation */
+    PD_ECUDA = -4,   /* any other CUDA runtime failure */
+    PD_ENODEV = -5   /* no CUDA device, or not an sm_100 part */
+} pd_status;
+
+typedef enum pd_path {
+    PD_PATH_GRAY = 0,  /* K1 diagonal gather + K2 Gray-code FP64 sum (the paper's O(8^N) method) */
+    PD_PATH_WHT = 1,   /* K1 + fast Walsh-Hadamard butterflies (separately reported second path) */
+    PD_PATH_NAIVE = 2  /* K0: one thread per n, reference-order walk straight from G */
+} pd_path;
+
+typedef struct pd_ctx pd_ctx;
+
+PD_EXPORT const char* pd_last_error(void);
+PD_EXPORT int pd_api_version(void);
+
+/* Device context: binds a CUDA device and owns a stream plus cached scratch.
+ * One host thread per context (the reference's calls are synchronous). */
+PD_EXPORT int pd_ctx_create(int device, pd_ctx** out);
+PD_EXPORT int pd_ctx_destroy(pd_ctx* ctx);
+/* the context's stream, as a cudaStream_t */
+PD_EXPORT void* pd_ctx_stream(pd_ctx* ctx);
+
+/* ---------------- host-buffer entry points (synchronous) ---------------- */
+
+/* All 4^N coefficients of the 2^N x 2^N matrix g, written to out (2*4^N doubles).
+ * Replaces decompose_parallel(const DenseMatrix&, unsigned threads)
+ * (decompose.hpp:46, decompose.cpp:95-131,205-207) and
+ * decompose_serial_quaternary (decompose.hpp:55; same output). */
+PD_EXPORT int pd_decompose(pd_ctx* ctx, unsigned num_qubits, const double* g, double* out, pd_path path);
+
+/* One coefficient c_n, written to out[0..1].
+ * Replaces coeff_fast(const DenseMatrix&, uint64_t n) (decompose.hpp:33,
+ * decompose.cpp:49-57,156-159); slow != 0 replaces coeff_slow (decompose.hpp:35). */
+PD_EXPORT int pd_coeff(pd_ctx* ctx, unsigned num_qubits, const double* g, uint64_t n, int slow, double* out);
+
+/* Many coefficients of one matrix: out[2k..2k+1] = c_{ns[k]}. Batched form of
+ * coeff_fast (decompose.hpp:33), one call instead of `count` calls. */
+PD_EXPORT int pd_coeff_batch(pd_ctx* ctx, unsigned num_qubits, const double* g, const uint64_t* ns,
+                   uint64_t count, double* out);
+
+/* Brute-force Kronecker-product trace Tr(P_n G)/2^N, N <= 6.
+ * Replaces oracle_coeff_kron (decompose.hpp:37, decompose.cpp:176-203). */
+PD_EXPORT int pd_oracle_coeff(pd_ctx* ctx, unsigned num_qubits, const double* g, uint64_t n, double* out);
+
+/* Dense matrix sum_n c_n P_n from all 4^N coefficients (2*4^N doubles) into g_out
+ * (2*4^N doubles). Replaces recompose(const PauliDecomposition&) (decompose.hpp:59,
+ * decompose.cpp:221-250). N <= 16. */
+PD_EXPORT int pd_recompose(pd_ctx* ctx, unsigned num_qubits, const double* coeffs, double* g_out);
+
+/* ---------------- device-resident entry points (stream-ordered) ---------------- */
+
+/* Scratch bytes pd_decompose_device needs for `path` (0 for PD_PATH_NAIVE). */
+PD_EXPORT uint64_t pd_scratch_bytes(unsigned num_qubits, uint64_t x_count, pd_path path);
+
+/* Full decomposition of a device-resident matrix into a device coefficient array,
+ * using caller-provided scratch (>= pd_scratch_bytes(N, 2^N, path)). */
+PD_EXPORT int pd_decompose_device(unsigned num_qubits, const double* g, double* out, void* scratch,
+                        pd_path path, void* stream);
+
+/* K1: diag[(x - x0) * dim + i] = G[i ^ x][i] for x in [x0, x0 + x_count).
+ * x_count is a power of two and x0 a multiple of it. */
+PD_EXPORT int pd_diag_gather_device(unsigned num_qubits, const double* g, uint64_t x0, uint64_t x_count,
+                          double* diag, void* stream);
+
+/* K2 (path GRAY) or K4 (path WHT): every coefficient whose X-mask lies in
+ * [x0, x0 + x_count), from the gathered diagonals. Output addressing follows the
+ * X-mask sharding of the multi-GPU layer: with run_bits = p, X-mask shard
+ * g = x0 >> (N - p) owns 2^p contiguous runs of 4^(N-p) coefficients of the
+ * reference-ordered array, one per value of the top p bits of the Z-mask;
+ * run_out[r] receives the run for Z-mask top bits r (2^p device pointers).
+ * p = 0 with run_out[0] = out writes the plain reference-ordered array. */
+PD_EXPORT int pd_xmask_coeffs_device(unsigned num_qubits, const double* diag, uint64_t x0, uint64_t x_count,
+                           unsigned run_bits, double* const* run_out, pd_path path, void* stream);
+
+/* Global offset (in coefficients) of run r of X-mask shard g for p = run_bits. */
+PD_EXPORT uint64_t pd_run_offset(unsigned num_qubits, unsigned run_bits, uint64_t shard, uint64_t run);
+
+/* Device form of pd_recompose; scratch >= 16 * 4^N bytes. */
+PD_EXPORT int pd_recompose_device(unsigned num_qubits, const double* coeffs, double* g_out, void* scratch,
+                        void* stream);
+
+/* K3: out[k] = c_{ns[k]} for a device list of tensor numbers (reference-order walk). */
+PD_EXPORT int pd_coeff_batch_device(unsigned num_qubits, const double* g, const uint64_t* ns, uint64_t count,
+                          int slow, double* out, void* stream);
+
+/* Device restatement of the reference's seeded generator random_matrix(N, seed)
+ * (bench.cpp:16-58); bit-identical to it. */
+PD_EXPORT int pd_random_matrix_device(unsigned num_qubits, uint64_t seed, double* g, void* stream);
+
+/* ---------------- measurement helpers ---------------- */
+
+/* Number of kernels this library has launched in this process (all threads). */
+PD_EXPORT uint64_t pd_launch_count(void);
+
+/* FP64-add issue probe: runs a pure-DADD kernel over all SMs on the context's
+ * device and returns the achieved DADD/s in *dadd_per_s. */
+PD_EXPORT int pd_fp64_add_probe(pd_ctx* ctx, double* dadd_per_s);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PD_API_H */

@@ -1,0 +1,276 @@
+// paulidecomp.cpp — the reference's C++ API (include/paulidecomp_b200/decompose.hpp) over the
+// C ABI of include/pd_api.h. Host logic only: validation, exception mapping, label algebra.
+// All arithmetic on matrices and coefficients happens in the CUDA kernels.
+#include "paulidecomp_b200/decompose.hpp"
+
+#include <bit>
+#include <memory>
+#include <mutex>
+#include <new>
+#include <string>
+#include <unordered_map>
+
+#include "pd_api.h"
+
+namespace paulidecomp {
+
+namespace {
+
+// pd_status -> the reference's exception types (decompose.cpp:14-19, matrix.cpp:10-19)
+void raise(int rc) {
+    const std::string msg = pd_last_error();
+    switch (rc) {
+        case PD_OK: return;
+        case PD_EINVAL: throw std::invalid_argument(msg);
+        case PD_ELENGTH: throw std::length_error(msg);
+        case PD_ENOMEM: throw std::bad_alloc();
+        default: throw std::runtime_error(msg);
+    }
+}
+
+// one lazily created context per device; calls on a context are serialised
+struct Device {
+    std::mutex mu;
+    pd_ctx* ctx = nullptr;
+};
+
+std::mutex g_devices_mu;
+std::unordered_map<int, std::unique_ptr<Device>> g_devices;
+thread_local int t_device = 0;
+
+struct Lease {
+    std::unique_lock<std::mutex> lock;
+    pd_ctx* ctx;
+};
+
+Lease lease() {
+    Device* d;
+    {
+        std::lock_guard<std::mutex> g(g_devices_mu);
+        auto& slot = g_devices[t_device];
+        if (!slot) slot = std::make_unique<Device>();
+        d = slot.get();
+    }
+    std::unique_lock<std::mutex> lock(d->mu);
+    if (!d->ctx) raise(pd_ctx_create(t_device, &d->ctx));
+    return Lease{std::move(lock), d->ctx};
+}
+
+const double* as_doubles(const Complex* p) { return reinterpret_cast<const double*>(p); }
+double* as_doubles(Complex* p) { return reinterpret_cast<double*>(p); }
+
+void check_qubit_count(unsigned num_qubits) {  // matrix.cpp:10-19
+    if (num_qubits == 0) throw std::invalid_argument("a matrix needs at least one qubit (2x2)");
+    if (num_qubits > kMaxQubits)
+        throw std::invalid_argument("qubit count " + std::to_string(num_qubits) +
+                                    " exceeds the word-size bound of 32");
+    if (num_qubits >= 32)
+        throw std::length_error("dense storage for 32 qubits exceeds the address space");
+}
+
+void check_index(unsigned num_qubits, std::uint64_t n) {  // decompose.cpp:14-19
+    if (num_qubits < 32 && n >= (std::uint64_t{1} << (2 * num_qubits)))
+        throw std::invalid_argument("tensor number " + std::to_string(n) + " out of range for " +
+                                    std::to_string(num_qubits) + " qubits");
+}
+
+// closed-form multiplication counts of the reference kernels (proj/README.md:113-120)
+std::uint64_t fast_mults(unsigned N) { return N + 2 * (std::uint64_t{1} << N) - 1; }
+
+}  // namespace
+
+// ---------------- DenseMatrix (matrix.hpp:14-43 semantics) ----------------
+
+DenseMatrix::DenseMatrix(unsigned num_qubits) : num_qubits_(num_qubits) {
+    check_qubit_count(num_qubits);
+    elements_.assign(std::uint64_t{1} << (2 * num_qubits), Complex{0.0, 0.0});
+}
+
+DenseMatrix::DenseMatrix(unsigned num_qubits, std::vector<Complex> elements)
+    : num_qubits_(num_qubits), elements_(std::move(elements)) {
+    check_qubit_count(num_qubits);
+    const std::uint64_t want = std::uint64_t{1} << (2 * num_qubits);
+    if (elements_.size() != want)
+        throw std::invalid_argument("element buffer holds " + std::to_string(elements_.size()) +
+                                    " entries, expected " + std::to_string(want));
+}
+
+DenseMatrix DenseMatrix::identity(unsigned num_qubits) {
+    DenseMatrix m(num_qubits);
+    for (std::uint64_t i = 0; i < m.dim(); ++i) m(i, i) = Complex{1.0, 0.0};
+    return m;
+}
+
+// ---------------- views ----------------
+
+void set_device(int device) { t_device = device; }
+
+unsigned qubits_for_dim(std::uint64_t rows, std::uint64_t cols) {  // module.cpp:24-30
+    if (rows != cols || rows < 2 || !std::has_single_bit(rows))
+        throw std::invalid_argument("matrix must be square with power-of-two dimension >= 2");
+    return static_cast<unsigned>(std::countr_zero(rows));
+}
+
+void decompose_into(const Complex* g, unsigned num_qubits, Complex* out, Path path) {
+    check_qubit_count(num_qubits);
+    Lease l = lease();
+    raise(pd_decompose(l.ctx, num_qubits, as_doubles(g), as_doubles(out),
+                       static_cast<pd_path>(static_cast<int>(path))));
+}
+
+void coeff_batch_into(const Complex* g, unsigned num_qubits, const std::uint64_t* ns,
+                      std::uint64_t count, Complex* out) {
+    check_qubit_count(num_qubits);
+    for (std::uint64_t k = 0; k < count; ++k) check_index(num_qubits, ns[k]);
+    Lease l = lease();
+    raise(pd_coeff_batch(l.ctx, num_qubits, as_doubles(g), ns, count, as_doubles(out)));
+}
+
+Complex coeff_view(const Complex* g, unsigned num_qubits, std::uint64_t n, bool slow) {
+    check_qubit_count(num_qubits);
+    check_index(num_qubits, n);
+    double out[2];
+    Lease l = lease();
+    raise(pd_coeff(l.ctx, num_qubits, as_doubles(g), n, slow ? 1 : 0, out));
+    return Complex{out[0], out[1]};
+}
+
+Complex oracle_coeff_view(const Complex* g, unsigned num_qubits, std::uint64_t n) {
+    check_qubit_count(num_qubits);
+    check_index(num_qubits, n);
+    if (num_qubits > kOracleMaxQubits)
+        throw std::invalid_argument("reference path is capped at " +
+                                    std::to_string(kOracleMaxQubits) + " qubits");
+    double out[2];
+    Lease l = lease();
+    raise(pd_oracle_coeff(l.ctx, num_qubits, as_doubles(g), n, out));
+    return Complex{out[0], out[1]};
+}
+
+// ---------------- reference API ----------------
+
+Complex coeff_fast(const DenseMatrix& g, std::uint64_t n) {
+    return coeff_view(g.data(), g.num_qubits(), n, false);
+}
+
+Complex coeff_fast(const DenseMatrix& g, std::uint64_t n, MultCount& count) {
+    const Complex c = coeff_fast(g, n);
+    count.mults += fast_mults(g.num_qubits());
+    return c;
+}
+
+Complex coeff_slow(const DenseMatrix& g, std::uint64_t n) {
+    return coeff_view(g.data(), g.num_qubits(), n, true);
+}
+
+Complex coeff_slow(const DenseMatrix& g, std::uint64_t n, MultCount& count) {
+    const Complex c = coeff_slow(g, n);
+    count.mults += (g.num_qubits() + 1) * g.dim();
+    return c;
+}
+
+Complex oracle_coeff_kron(const DenseMatrix& g, std::uint64_t n) {
+    return oracle_coeff_view(g.data(), g.num_qubits(), n);
+}
+
+PauliDecomposition decompose(const DenseMatrix& g, Path path) {
+    PauliDecomposition d{g.num_qubits(), std::vector<Complex>(g.element_count())};
+    decompose_into(g.data(), g.num_qubits(), d.coefficients.data(), path);
+    return d;
+}
+
+PauliDecomposition decompose_parallel(const DenseMatrix& g, unsigned threads) {
+    if (threads == 0) throw std::invalid_argument("thread count must be at least 1");
+    return decompose(g, Path::Gray);
+}
+
+PauliDecomposition decompose_parallel(const DenseMatrix& g, unsigned threads, MultCount& count) {
+    PauliDecomposition d = decompose_parallel(g, threads);
+    count.mults += g.element_count() * fast_mults(g.num_qubits());
+    return d;
+}
+
+PauliDecomposition decompose_serial_quaternary(const DenseMatrix& g) {
+    // same coefficients (the reference's quaternary walk is bit-identical to its parallel one)
+    return decompose(g, Path::Gray);
+}
+
+PauliDecomposition decompose_serial_quaternary(const DenseMatrix& g, MultCount& count) {
+    PauliDecomposition d = decompose_serial_quaternary(g);
+    const std::uint64_t strings = g.element_count();
+    count.mults += g.num_qubits() + strings * (2 * g.dim() - 1) + (strings - 1);
+    return d;
+}
+
+std::vector<Complex> coeff_batch(const DenseMatrix& g, const std::vector<std::uint64_t>& ns) {
+    std::vector<Complex> out(ns.size());
+    coeff_batch_into(g.data(), g.num_qubits(), ns.data(), ns.size(), out.data());
+    return out;
+}
+
+DenseMatrix recompose(const PauliDecomposition& d) {  // decompose.cpp:221-230 validation
+    if (d.num_qubits == 0 || d.num_qubits > kMaxQubits)
+        throw std::invalid_argument("qubit count must be in [1, 32]");
+    if (d.num_qubits == kMaxQubits)
+        throw std::length_error("a dense matrix for N=32 exceeds the address space");
+    const std::uint64_t want = std::uint64_t{1} << (2 * d.num_qubits);
+    if (d.coefficients.size() != want)
+        throw std::invalid_argument("coefficient array holds " +
+                                    std::to_string(d.coefficients.size()) + " entries, expected " +
+                                    std::to_string(want));
+    DenseMatrix out(d.num_qubits);
+    Lease l = lease();
+    raise(pd_recompose(l.ctx, d.num_qubits, as_doubles(d.coefficients.data()), as_doubles(out.data())));
+    return out;
+}
+
+// ---------------- labels and bit utilities (pauli_string.cpp:25-54, bits.hpp, pauli.hpp) ----
+
+std::uint64_t string_to_index(std::string_view label, unsigned num_qubits) {
+    if (num_qubits == 0 || num_qubits > kMaxQubits)
+        throw FormatError("operator count must be in [1, 32], got " + std::to_string(num_qubits));
+    if (label.size() != num_qubits)
+        throw FormatError("label \"" + std::string(label) + "\" has " +
+                          std::to_string(label.size()) + " characters, expected " +
+                          std::to_string(num_qubits));
+    std::uint64_t n = 0;
+    for (unsigned t = 0; t < num_qubits; ++t) {  // digit 0 is the rightmost character
+        unsigned code;
+        switch (label[num_qubits - 1 - t]) {
+            case 'I': code = 0; break;
+            case 'X': code = 1; break;
+            case 'Y': code = 2; break;
+            case 'Z': code = 3; break;
+            default:
+                throw FormatError("label \"" + std::string(label) +
+                                  "\" contains a character outside IXYZ");
+        }
+        n |= std::uint64_t{code} << (2 * t);
+    }
+    return n;
+}
+
+std::string index_to_string(std::uint64_t n, unsigned num_qubits) {
+    if (num_qubits == 0 || num_qubits > kMaxQubits)
+        throw std::invalid_argument("operator count must be in [1, 32]");
+    check_index(num_qubits, n);
+    static constexpr char kOps[4] = {'I', 'X', 'Y', 'Z'};
+    std::string label(num_qubits, 'I');
+    for (unsigned t = 0; t < num_qubits; ++t) label[num_qubits - 1 - t] = kOps[(n >> (2 * t)) & 3u];
+    return label;
+}
+
+std::uint64_t xy_mask(std::uint64_t n, unsigned num_qubits) {
+    std::uint64_t mask = 0;
+    for (unsigned t = 0; t < num_qubits && t < kMaxQubits; ++t) {
+        const unsigned d = (n >> (2 * t)) & 3u;
+        mask |= std::uint64_t{(d ^ (d >> 1)) & 1u} << t;
+    }
+    return mask;
+}
+
+std::uint64_t gray_code(std::uint64_t k) { return k ^ (k >> 1); }
+
+unsigned flipped_bit_index(std::uint64_t k) { return static_cast<unsigned>(std::countr_zero(k + 1)); }
+
+}  // namespace paulidecomp

@@ -1,0 +1,422 @@
+// pd_api.cu — implementation of the C ABI in include/pd_api.h.
+//
+// Validation and error codes mirror the reference's contract:
+//   * N outside [1, 32]           -> PD_EINVAL  (matrix.cpp:10-15 check_qubit_count)
+//   * N == 32                     -> PD_ELENGTH (matrix.cpp:17-18)
+//   * n >= 4^N                    -> PD_EINVAL  (decompose.cpp:14-19 check_index)
+//   * oracle with N > 6           -> PD_EINVAL  (decompose.cpp:179-181, kOracleMaxQubits)
+// There is no CPU path: without an sm_100 device every compute call is PD_ENODEV.
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "pd_api.h"
+#include "pd_kernels.h"
+
+namespace {
+
+thread_local std::string t_error;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    std::vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    t_error = buf;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    cudaGetLastError();  // clear sticky-free errors
+    return fail(e == cudaErrorMemoryAllocation ? PD_ENOMEM : PD_ECUDA, "%s: %s", what,
+                cudaGetErrorString(e));
+}
+
+#define PD_CUDA(call)                                       \
+    do {                                                    \
+        cudaError_t _e = (call);                            \
+        if (_e != cudaSuccess) return cuda_fail(_e, #call); \
+    } while (0)
+
+constexpr unsigned kMaxQubits = 32;      // bits.hpp:15
+constexpr unsigned kOracleMaxQubits = 6; // decompose.hpp:11
+
+int check_qubits(unsigned N) {
+    if (N == 0) return fail(PD_EINVAL, "a matrix needs at least one qubit (2x2)");
+    if (N > kMaxQubits)
+        return fail(PD_EINVAL, "qubit count %u exceeds the word-size bound of 32", N);
+    if (N >= 32) return fail(PD_ELENGTH, "dense storage for 32 qubits exceeds the address space");
+    return PD_OK;
+}
+
+int check_index(unsigned N, uint64_t n) {
+    if (N < 32 && n >= (1ull << (2 * N)))
+        return fail(PD_EINVAL, "tensor number %llu out of range for %u qubits",
+                    static_cast<unsigned long long>(n), N);
+    return PD_OK;
+}
+
+int check_device() {
+    static std::once_flag once;
+    static int status = PD_OK;
+    static std::string msg;
+    std::call_once(once, [] {
+        int count = 0;
+        cudaError_t e = cudaGetDeviceCount(&count);
+        if (e != cudaSuccess || count == 0) {
+            cudaGetLastError();
+            status = PD_ENODEV;
+            msg = std::string("no CUDA device available (") + cudaGetErrorString(e) +
+                  "); this library has no CPU path";
+            return;
+        }
+        int dev = 0, major = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+        if (major != 10) {
+            status = PD_ENODEV;
+            msg = "device is not an sm_100 (Blackwell B200) part; kernels are built for sm_100a only";
+        }
+    });
+    if (status != PD_OK) return fail(status, "%s", msg.c_str());
+    return PD_OK;
+}
+
+uint64_t elems(unsigned N) { return 1ull << (2 * N); }
+
+}  // namespace
+
+struct pd_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    void* g = nullptr;
+    size_t g_bytes = 0;
+    void* out = nullptr;
+    size_t out_bytes = 0;
+    void* scratch = nullptr;
+    size_t scratch_bytes = 0;
+    void* ns = nullptr;
+    size_t ns_bytes = 0;
+
+    int ensure(void** p, size_t* have, size_t need) {
+        if (*have >= need) return PD_OK;
+        if (*p) cudaFree(*p);
+        *p = nullptr;
+        *have = 0;
+        cudaError_t e = cudaMalloc(p, need);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+        *have = need;
+        return PD_OK;
+    }
+};
+
+namespace {
+
+// Copy to/from a host buffer; cudaMemcpyAsync handles both pinned (DMA straight
+// from the caller's buffer) and pageable memory (driver-staged).
+int upload(pd_ctx* ctx, void* dst, const void* src, size_t bytes) {
+    PD_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    return PD_OK;
+}
+
+int bind(pd_ctx* ctx) {
+    if (!ctx) return fail(PD_EINVAL, "null context");
+    PD_CUDA(cudaSetDevice(ctx->device));
+    return PD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* pd_last_error(void) { return t_error.c_str(); }
+
+int pd_api_version(void) { return PD_API_VERSION; }
+
+uint64_t pd_launch_count(void) { return pdb::g_launches.load(); }
+
+int pd_ctx_create(int device, pd_ctx** out) {
+    if (!out) return fail(PD_EINVAL, "null output pointer");
+    *out = nullptr;
+    if (int rc = check_device()) return rc;
+    int count = 0;
+    PD_CUDA(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count)
+        return fail(PD_EINVAL, "device %d out of range (%d devices)", device, count);
+    PD_CUDA(cudaSetDevice(device));
+    pd_ctx* ctx = new pd_ctx();
+    ctx->device = device;
+    cudaError_t e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        delete ctx;
+        return cuda_fail(e, "cudaStreamCreate");
+    }
+    *out = ctx;
+    return PD_OK;
+}
+
+int pd_ctx_destroy(pd_ctx* ctx) {
+    if (!ctx) return PD_OK;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    for (void* p : {ctx->g, ctx->out, ctx->scratch, ctx->ns})
+        if (p) cudaFree(p);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return PD_OK;
+}
+
+void* pd_ctx_stream(pd_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+uint64_t pd_scratch_bytes(unsigned N, uint64_t x_count, pd_path path) {
+    if (N == 0 || N >= 32 || path == PD_PATH_NAIVE) return 0;
+    return x_count * (1ull << N) * sizeof(double2);
+}
+
+uint64_t pd_run_offset(unsigned N, unsigned run_bits, uint64_t shard, uint64_t run) {
+    // top run_bits digits: d_t = 2 z_t + (x_t ^ z_t) with x's top bits = shard, z's = run
+    const unsigned low = N - run_bits;
+    uint64_t top = 0;
+    for (unsigned t = 0; t < run_bits; ++t) {
+        const uint64_t xt = (shard >> t) & 1, zt = (run >> t) & 1;
+        top |= (2 * zt + (xt ^ zt)) << (2 * t);
+    }
+    return top << (2 * low);
+}
+
+int pd_diag_gather_device(unsigned N, const double* g, uint64_t x0, uint64_t x_count,
+                          double* diag, void* stream) {
+    if (int rc = check_qubits(N)) return rc;
+    if (int rc = check_device()) return rc;
+    if (x_count == 0 || (x_count & (x_count - 1)) || x0 % x_count || x0 + x_count > (1ull << N))
+        return fail(PD_EINVAL, "X-mask range must be an aligned power-of-two block inside [0, 2^N)");
+    cudaError_t e = pdb::launch_diag_gather(reinterpret_cast<const double2*>(g), N, x0, x_count,
+                                            reinterpret_cast<double2*>(diag),
+                                            static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "diag_gather launch");
+    return PD_OK;
+}
+
+int pd_xmask_coeffs_device(unsigned N, const double* diag, uint64_t x0, uint64_t x_count,
+                           unsigned run_bits, double* const* run_out, pd_path path, void* stream) {
+    if (int rc = check_qubits(N)) return rc;
+    if (int rc = check_device()) return rc;
+    if (run_bits > pdb::kMaxRunBits || run_bits > N)
+        return fail(PD_EINVAL, "run_bits must be <= min(3, N)");
+    if (x_count == 0 || (x_count & (x_count - 1)) || x0 % x_count || x0 + x_count > (1ull << N))
+        return fail(PD_EINVAL, "X-mask range must be an aligned power-of-two block inside [0, 2^N)");
+    if (x_count > (1ull << (N - run_bits)))
+        return fail(PD_EINVAL, "X-mask range spans more than one shard");
+    if (!run_out) return fail(PD_EINVAL, "null run_out");
+    double2* runs[pdb::kMaxRuns] = {};
+    for (unsigned r = 0; r < (1u << run_bits); ++r) {
+        if (!run_out[r]) return fail(PD_EINVAL, "null run_out[%u]", r);
+        runs[r] = reinterpret_cast<double2*>(run_out[r]);
+    }
+    cudaError_t e;
+    const double2* d = reinterpret_cast<const double2*>(diag);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    switch (path) {
+        case PD_PATH_GRAY: e = pdb::launch_gray_xmask(d, N, x0, x_count, run_bits, runs, s); break;
+        case PD_PATH_WHT:
+            if (N > 16) return fail(PD_EINVAL, "the WHT path supports N <= 16");
+            e = pdb::launch_wht_xmask(d, N, x0, x_count, run_bits, runs, s);
+            break;
+        default: return fail(PD_EINVAL, "path must be PD_PATH_GRAY or PD_PATH_WHT");
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "xmask coefficient launch");
+    return PD_OK;
+}
+
+int pd_decompose_device(unsigned N, const double* g, double* out, void* scratch, pd_path path,
+                        void* stream) {
+    if (int rc = check_qubits(N)) return rc;
+    if (int rc = check_device()) return rc;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (path == PD_PATH_NAIVE) {
+        cudaError_t e = pdb::launch_walk(reinterpret_cast<const double2*>(g), N, nullptr, elems(N),
+                                         false, reinterpret_cast<double2*>(out), s);
+        if (e != cudaSuccess) return cuda_fail(e, "walk launch");
+        return PD_OK;
+    }
+    if (path != PD_PATH_GRAY && path != PD_PATH_WHT) return fail(PD_EINVAL, "unknown path");
+    if (!scratch) return fail(PD_EINVAL, "null scratch");
+    const uint64_t dim = 1ull << N;
+    if (int rc = pd_diag_gather_device(N, g, 0, dim, static_cast<double*>(scratch), stream)) return rc;
+    double* runs[1] = {out};
+    return pd_xmask_coeffs_device(N, static_cast<const double*>(scratch), 0, dim, 0, runs, path,
+                                  stream);
+}
+
+int pd_coeff_batch_device(unsigned N, const double* g, const uint64_t* ns, uint64_t count, int slow,
+                          double* out, void* stream) {
+    if (int rc = check_qubits(N)) return rc;
+    if (int rc = check_device()) return rc;
+    cudaError_t e = pdb::launch_walk(reinterpret_cast<const double2*>(g), N, ns, count, slow != 0,
+                                     reinterpret_cast<double2*>(out),
+                                     static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "walk launch");
+    return PD_OK;
+}
+
+int pd_recompose_device(unsigned N, const double* coeffs, double* g_out, void* scratch,
+                        void* stream) {
+    if (int rc = check_qubits(N)) return rc;
+    if (int rc = check_device()) return rc;
+    if (N > 16) return fail(PD_EINVAL, "recompose supports N <= 16");
+    if (!coeffs || !g_out || !scratch) return fail(PD_EINVAL, "null buffer");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    double2* rows = static_cast<double2*>(scratch);
+    cudaError_t e = pdb::launch_recompose_gather(reinterpret_cast<const double2*>(coeffs), N, rows, s);
+    if (e == cudaSuccess) e = pdb::launch_wht_inplace(rows, N, 1ull << N, s);
+    if (e == cudaSuccess)
+        e = pdb::launch_recompose_scatter(rows, N, reinterpret_cast<double2*>(g_out), s);
+    if (e != cudaSuccess) return cuda_fail(e, "recompose launch");
+    return PD_OK;
+}
+
+int pd_random_matrix_device(unsigned N, uint64_t seed, double* g, void* stream) {
+    if (int rc = check_qubits(N)) return rc;
+    if (int rc = check_device()) return rc;
+    cudaError_t e = pdb::launch_random_matrix(N, seed, reinterpret_cast<double2*>(g),
+                                              static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "random_matrix launch");
+    return PD_OK;
+}
+
+// ---------------- host-buffer entry points ----------------
+
+int pd_decompose(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_path path) {
+    if (int rc = check_qubits(N)) return rc;
+    if (int rc = bind(ctx)) return rc;
+    if (!g || !out) return fail(PD_EINVAL, "null buffer");
+    const size_t bytes = elems(N) * sizeof(double2);
+    if (int rc = ctx->ensure(&ctx->g, &ctx->g_bytes, bytes)) return rc;
+    if (int rc = ctx->ensure(&ctx->out, &ctx->out_bytes, bytes)) return rc;
+    const uint64_t sb = pd_scratch_bytes(N, 1ull << N, path);
+    if (sb && (ctx->ensure(&ctx->scratch, &ctx->scratch_bytes, sb) != PD_OK)) return PD_ENOMEM;
+    if (int rc = upload(ctx, ctx->g, g, bytes)) return rc;
+    if (int rc = pd_decompose_device(N, static_cast<const double*>(ctx->g),
+                                     static_cast<double*>(ctx->out), ctx->scratch, path,
+                                     ctx->stream))
+        return rc;
+    PD_CUDA(cudaMemcpyAsync(out, ctx->out, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    PD_CUDA(cudaStreamSynchronize(ctx->stream));
+    return PD_OK;
+}
+
+int pd_recompose(pd_ctx* ctx, unsigned N, const double* coeffs, double* g_out) {
+    if (int rc = check_qubits(N)) return rc;
+    if (int rc = bind(ctx)) return rc;
+    if (!coeffs || !g_out) return fail(PD_EINVAL, "null buffer");
+    const size_t bytes = elems(N) * sizeof(double2);
+    if (int rc = ctx->ensure(&ctx->g, &ctx->g_bytes, bytes)) return rc;
+    if (int rc = ctx->ensure(&ctx->out, &ctx->out_bytes, bytes)) return rc;
+    if (int rc = ctx->ensure(&ctx->scratch, &ctx->scratch_bytes, bytes)) return rc;
+    if (int rc = upload(ctx, ctx->out, coeffs, bytes)) return rc;
+    if (int rc = pd_recompose_device(N, static_cast<const double*>(ctx->out),
+                                     static_cast<double*>(ctx->g), ctx->scratch, ctx->stream))
+        return rc;
+    PD_CUDA(cudaMemcpyAsync(g_out, ctx->g, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    PD_CUDA(cudaStreamSynchronize(ctx->stream));
+    return PD_OK;
+}
+
+int pd_coeff_batch(pd_ctx* ctx, unsigned N, const double* g, const uint64_t* ns, uint64_t count,
+                   double* out) {
+    if (int rc = check_qubits(N)) return rc;
+    for (uint64_t k = 0; k < count; ++k)
+        if (int rc = check_index(N, ns[k])) return rc;
+    if (int rc = bind(ctx)) return rc;
+    if (count == 0) return PD_OK;
+    const size_t gbytes = elems(N) * sizeof(double2);
+    if (int rc = ctx->ensure(&ctx->g, &ctx->g_bytes, gbytes)) return rc;
+    if (int rc = ctx->ensure(&ctx->ns, &ctx->ns_bytes, count * sizeof(uint64_t))) return rc;
+    if (int rc = ctx->ensure(&ctx->out, &ctx->out_bytes, count * sizeof(double2))) return rc;
+    if (int rc = upload(ctx, ctx->g, g, gbytes)) return rc;
+    if (int rc = upload(ctx, ctx->ns, ns, count * sizeof(uint64_t))) return rc;
+    if (int rc = pd_coeff_batch_device(N, static_cast<const double*>(ctx->g),
+                                       static_cast<const uint64_t*>(ctx->ns), count, 0,
+                                       static_cast<double*>(ctx->out), ctx->stream))
+        return rc;
+    PD_CUDA(cudaMemcpyAsync(out, ctx->out, count * sizeof(double2), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    PD_CUDA(cudaStreamSynchronize(ctx->stream));
+    return PD_OK;
+}
+
+int pd_coeff(pd_ctx* ctx, unsigned N, const double* g, uint64_t n, int slow, double* out) {
+    if (int rc = check_qubits(N)) return rc;
+    if (int rc = check_index(N, n)) return rc;
+    if (int rc = bind(ctx)) return rc;
+    const size_t gbytes = elems(N) * sizeof(double2);
+    if (int rc = ctx->ensure(&ctx->g, &ctx->g_bytes, gbytes)) return rc;
+    if (int rc = ctx->ensure(&ctx->ns, &ctx->ns_bytes, sizeof(uint64_t))) return rc;
+    if (int rc = ctx->ensure(&ctx->out, &ctx->out_bytes, sizeof(double2))) return rc;
+    if (int rc = upload(ctx, ctx->g, g, gbytes)) return rc;
+    if (int rc = upload(ctx, ctx->ns, &n, sizeof(uint64_t))) return rc;
+    // the pageable source of the 8-byte index must stay valid until the copy runs
+    PD_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (int rc = pd_coeff_batch_device(N, static_cast<const double*>(ctx->g),
+                                       static_cast<const uint64_t*>(ctx->ns), 1, slow,
+                                       static_cast<double*>(ctx->out), ctx->stream))
+        return rc;
+    PD_CUDA(cudaMemcpyAsync(out, ctx->out, sizeof(double2), cudaMemcpyDeviceToHost, ctx->stream));
+    PD_CUDA(cudaStreamSynchronize(ctx->stream));
+    return PD_OK;
+}
+
+int pd_oracle_coeff(pd_ctx* ctx, unsigned N, const double* g, uint64_t n, double* out) {
+    if (int rc = check_qubits(N)) return rc;
+    if (int rc = check_index(N, n)) return rc;
+    if (N > kOracleMaxQubits)
+        return fail(PD_EINVAL, "reference path is capped at %u qubits", kOracleMaxQubits);
+    if (int rc = bind(ctx)) return rc;
+    const size_t gbytes = elems(N) * sizeof(double2);
+    if (int rc = ctx->ensure(&ctx->g, &ctx->g_bytes, gbytes)) return rc;
+    if (int rc = ctx->ensure(&ctx->out, &ctx->out_bytes, sizeof(double2))) return rc;
+    if (int rc = upload(ctx, ctx->g, g, gbytes)) return rc;
+    cudaError_t e = pdb::launch_kron_trace(static_cast<const double2*>(ctx->g), N, n,
+                                           static_cast<double2*>(ctx->out), ctx->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "kron_trace launch");
+    PD_CUDA(cudaMemcpyAsync(out, ctx->out, sizeof(double2), cudaMemcpyDeviceToHost, ctx->stream));
+    PD_CUDA(cudaStreamSynchronize(ctx->stream));
+    return PD_OK;
+}
+
+int pd_fp64_add_probe(pd_ctx* ctx, double* dadd_per_s) {
+    if (int rc = bind(ctx)) return rc;
+    if (!dadd_per_s) return fail(PD_EINVAL, "null output");
+    int sms = 0;
+    PD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+    double* sink = nullptr;
+    PD_CUDA(cudaMalloc(&sink, sizeof(double)));
+    const unsigned blocks = static_cast<unsigned>(sms) * 8, iters = 1u << 15;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaError_t e = pdb::launch_fp64_probe(blocks, iters, sink, ctx->stream);  // warm-up
+    float ms = 0.f;
+    if (e == cudaSuccess) {
+        cudaEventRecord(a, ctx->stream);
+        e = pdb::launch_fp64_probe(blocks, iters, sink, ctx->stream);
+        cudaEventRecord(b, ctx->stream);
+        if (e == cudaSuccess) e = cudaEventSynchronize(b);
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, a, b);
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(sink);
+    if (e != cudaSuccess) return cuda_fail(e, "fp64 probe");
+    const double dadds = static_cast<double>(blocks) * 256.0 * 16.0 * iters;
+    *dadd_per_s = dadds / (ms * 1e-3);
+    return PD_OK;
+}
+
+}  // extern "C"

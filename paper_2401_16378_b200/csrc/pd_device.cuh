@@ -1,0 +1,128 @@
+// pd_device.cuh — device-side index algebra and PTX helpers shared by the kernels.
+//
+// Index algebra restated from the reference (paths relative to proj/):
+//   * tensor number n, base-4 digit d_t = (n >> 2t) & 3 selects sigma_t in
+//     {I,X,Y,Z} (pauli.hpp:13-20, bits.hpp:52-55);
+//   * X-mask x_t = [d_t in {X,Y}] (pauli.hpp:23-39 xy_mask), Z-mask z_t = d_t >> 1,
+//     so d_t = 2 z_t + (x_t ^ z_t);
+//   * c_n = 2^-N (-i)^{|x&z|} sum_k (-1)^{|g_k & z|} G[g_k ^ x][g_k], g_k = k ^ (k>>1):
+//     the reference's Gray walk (decompose.cpp:30-47) with lambda_0 = (-i)^{#Y}
+//     (pauli.hpp:97-102) and row-flip quotient -1 for Y,Z (pauli.hpp:65-68).
+#pragma once
+
+#include <cstdint>
+
+namespace pdb {
+
+// bit t of v -> bit 2t
+__host__ __device__ __forceinline__ uint64_t spread_bits(uint64_t v) {
+    v &= 0xFFFFFFFFull;
+    v = (v | (v << 16)) & 0x0000FFFF0000FFFFull;
+    v = (v | (v << 8)) & 0x00FF00FF00FF00FFull;
+    v = (v | (v << 4)) & 0x0F0F0F0F0F0F0F0Full;
+    v = (v | (v << 2)) & 0x3333333333333333ull;
+    v = (v | (v << 1)) & 0x5555555555555555ull;
+    return v;
+}
+
+// bit 2t of v -> bit t
+__host__ __device__ __forceinline__ uint64_t gather_even_bits(uint64_t v) {
+    v &= 0x5555555555555555ull;
+    v = (v | (v >> 1)) & 0x3333333333333333ull;
+    v = (v | (v >> 2)) & 0x0F0F0F0F0F0F0F0Full;
+    v = (v | (v >> 4)) & 0x00FF00FF00FF00FFull;
+    v = (v | (v >> 8)) & 0x0000FFFF0000FFFFull;
+    v = (v | (v >> 16)) & 0x00000000FFFFFFFFull;
+    return v;
+}
+
+// tensor number of the string with X-mask x and Z-mask z
+__host__ __device__ __forceinline__ uint64_t tensor_number(uint64_t x, uint64_t z) {
+    return spread_bits(x ^ z) | (spread_bits(z) << 1);
+}
+
+__host__ __device__ __forceinline__ uint64_t xmask_of(uint64_t n) {
+    return gather_even_bits(n ^ (n >> 1));
+}
+
+__host__ __device__ __forceinline__ uint64_t zmask_of(uint64_t n) { return gather_even_bits(n >> 1); }
+
+__host__ __device__ __forceinline__ uint64_t gray(uint64_t k) { return k ^ (k >> 1); }
+
+// parity of v; non-recursive so that it folds to a constant inside unrolled loops
+__host__ __device__ __forceinline__ constexpr int cparity(unsigned v) {
+    v ^= v >> 16;
+    v ^= v >> 8;
+    v ^= v >> 4;
+    v ^= v >> 2;
+    v ^= v >> 1;
+    return static_cast<int>(v & 1u);
+}
+
+__host__ __device__ constexpr unsigned cgray(unsigned k) { return k ^ (k >> 1); }
+
+// flip the sign of a double when sgn == 0x80000000 (exact, branchless)
+// (inline PTX keeps the front end from rewriting it as a select between v and a
+// negation, which would cost an extra FP64-pipe DNEG per element)
+__device__ __forceinline__ double flip_sign(double v, unsigned sgn) {
+    int hi = __double2hiint(v);
+    asm("xor.b32 %0, %0, %1;" : "+r"(hi) : "r"(sgn));
+    return __hiloint2double(hi, __double2loint(v));
+}
+
+// c = i^p * (sr + i si), then * scale (2^-N, exact). p = 3|x&z| mod 4 encodes (-i)^{|x&z|}.
+__device__ __forceinline__ double2 apply_phase(unsigned p, double sr, double si, double scale) {
+    double cr, ci;
+    switch (p & 3u) {
+        case 0: cr = sr; ci = si; break;
+        case 1: cr = -si; ci = sr; break;
+        case 2: cr = -sr; ci = -si; break;
+        default: cr = si; ci = -sr; break;
+    }
+    return make_double2(cr * scale, ci * scale);
+}
+
+// ---- mbarrier / bulk-copy (TMA engine) PTX ----
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+}
+
+__device__ __forceinline__ void fence_barrier_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+// 1-D bulk copy global -> shared through the TMA engine, completing on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "PD_WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra PD_WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+}  // namespace pdb

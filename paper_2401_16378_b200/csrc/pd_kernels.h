@@ -1,0 +1,52 @@
+// pd_kernels.h — host launchers of the kernels in pd_kernels.cu / pd_wht.cu (namespace pdb).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+
+namespace pdb {
+
+constexpr unsigned kMaxRunBits = 3;  // up to 8 X-mask shards (one 8xB200 box)
+constexpr unsigned kMaxRuns = 1u << kMaxRunBits;
+
+extern std::atomic<uint64_t> g_launches;
+
+// K1: diag[(x - x0) * 2^N + i] = G[i ^ x][i], x in [x0, x0 + x_count)
+cudaError_t launch_diag_gather(const double2* G, unsigned N, uint64_t x0, uint64_t x_count,
+                               double2* diag, cudaStream_t stream);
+
+// K2: Gray-code sums for the X-masks [x0, x0 + x_count); run addressing as in pd_api.h
+cudaError_t launch_gray_xmask(const double2* diag, unsigned N, uint64_t x0, uint64_t x_count,
+                              unsigned run_bits, double2* const* run_out, cudaStream_t stream);
+uint64_t gray_xmask_grid(unsigned N, uint64_t x_count);
+
+// K4: fast Walsh-Hadamard path over the same diagonals (separately reported)
+cudaError_t launch_wht_xmask(const double2* diag, unsigned N, uint64_t x0, uint64_t x_count,
+                             unsigned run_bits, double2* const* run_out, cudaStream_t stream);
+
+// in-place unnormalised Walsh-Hadamard transform of x_count rows of 2^N (N <= 16)
+cudaError_t launch_wht_inplace(double2* rows, unsigned N, uint64_t x_count, cudaStream_t stream);
+
+// recompose (decompose.cpp:221-250) on the device:
+//   gather   E[x][z] = (-i)^{|x&z|} c[n(x,z)]
+//   (WHT in place over z)
+//   scatter  G[row][col] = E[row ^ col][row]
+cudaError_t launch_recompose_gather(const double2* coeffs, unsigned N, double2* rows,
+                                    cudaStream_t stream);
+cudaError_t launch_recompose_scatter(const double2* rows, unsigned N, double2* G,
+                                     cudaStream_t stream);
+
+// K0/K3: one thread per tensor number (ns == nullptr: n = 0..count-1)
+cudaError_t launch_walk(const double2* G, unsigned N, const uint64_t* ns, uint64_t count, bool slow,
+                        double2* out, cudaStream_t stream);
+
+cudaError_t launch_kron_trace(const double2* G, unsigned N, uint64_t n, double2* out,
+                              cudaStream_t stream);
+
+cudaError_t launch_random_matrix(unsigned N, uint64_t seed, double2* out, cudaStream_t stream);
+
+cudaError_t launch_fp64_probe(unsigned blocks, unsigned iters, double* sink, cudaStream_t stream);
+
+}  // namespace pdb
