@@ -94,7 +94,12 @@ uint64_t elems(unsigned N) { return 1ull << (2 * N); }
 
 struct pd_ctx {
     int device = 0;
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr;   // H2D, K1, even X-mask blocks
+    cudaStream_t stream2 = nullptr;  // odd X-mask blocks (overlaps the previous block's tail)
+    cudaStream_t d2h = nullptr;      // coefficient download, overlapped with later blocks
+    static constexpr int kBlocks = 8;
+    cudaEvent_t gathered = nullptr;
+    cudaEvent_t block_done[kBlocks] = {};
     void* g = nullptr;
     size_t g_bytes = 0;
     void* out = nullptr;
@@ -153,8 +158,13 @@ int pd_ctx_create(int device, pd_ctx** out) {
     pd_ctx* ctx = new pd_ctx();
     ctx->device = device;
     cudaError_t e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->gathered, cudaEventDisableTiming);
+    for (int b = 0; e == cudaSuccess && b < pd_ctx::kBlocks; ++b)
+        e = cudaEventCreateWithFlags(&ctx->block_done[b], cudaEventDisableTiming);
     if (e != cudaSuccess) {
-        delete ctx;
+        pd_ctx_destroy(ctx);
         return cuda_fail(e, "cudaStreamCreate");
     }
     *out = ctx;
@@ -164,10 +174,15 @@ int pd_ctx_create(int device, pd_ctx** out) {
 int pd_ctx_destroy(pd_ctx* ctx) {
     if (!ctx) return PD_OK;
     cudaSetDevice(ctx->device);
-    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    for (cudaStream_t s : {ctx->stream, ctx->stream2, ctx->d2h})
+        if (s) cudaStreamSynchronize(s);
     for (void* p : {ctx->g, ctx->out, ctx->scratch, ctx->ns})
         if (p) cudaFree(p);
-    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    if (ctx->gathered) cudaEventDestroy(ctx->gathered);
+    for (cudaEvent_t ev : ctx->block_done)
+        if (ev) cudaEventDestroy(ev);
+    for (cudaStream_t s : {ctx->stream, ctx->stream2, ctx->d2h})
+        if (s) cudaStreamDestroy(s);
     delete ctx;
     return PD_OK;
 }
@@ -302,12 +317,45 @@ int pd_decompose(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_path 
     const uint64_t sb = pd_scratch_bytes(N, 1ull << N, path);
     if (sb && (ctx->ensure(&ctx->scratch, &ctx->scratch_bytes, sb) != PD_OK)) return PD_ENOMEM;
     if (int rc = upload(ctx, ctx->g, g, bytes)) return rc;
-    if (int rc = pd_decompose_device(N, static_cast<const double*>(ctx->g),
-                                     static_cast<double*>(ctx->out), ctx->scratch, path,
-                                     ctx->stream))
+    const uint64_t dim = 1ull << N;
+    if (path == PD_PATH_NAIVE || N < 10) {
+        if (int rc = pd_decompose_device(N, static_cast<const double*>(ctx->g),
+                                         static_cast<double*>(ctx->out), ctx->scratch, path,
+                                         ctx->stream))
+            return rc;
+        PD_CUDA(cudaMemcpyAsync(out, ctx->out, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+        PD_CUDA(cudaStreamSynchronize(ctx->stream));
+        return PD_OK;
+    }
+    // Pipelined: K1 over all X-masks, then K2 (or K4) in 8 X-mask blocks alternating over two
+    // streams; block q's coefficients (8 runs of 4^(N-3), pd_run_offset) are downloaded while
+    // later blocks compute, so only the last block's D2H is exposed.
+    double* dout = static_cast<double*>(ctx->out);
+    double* diag = static_cast<double*>(ctx->scratch);
+    if (int rc = pd_diag_gather_device(N, static_cast<const double*>(ctx->g), 0, dim, diag, ctx->stream))
         return rc;
-    PD_CUDA(cudaMemcpyAsync(out, ctx->out, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    PD_CUDA(cudaEventRecord(ctx->gathered, ctx->stream));
+    PD_CUDA(cudaStreamWaitEvent(ctx->stream2, ctx->gathered, 0));
+    constexpr unsigned kBits = 3;
+    const uint64_t xc = dim >> kBits;
+    const uint64_t run = 1ull << (2 * (N - kBits));
+    double* runs[1] = {dout};
+    for (unsigned q = 0; q < (1u << kBits); ++q) {
+        cudaStream_t s = (q & 1) ? ctx->stream2 : ctx->stream;
+        // the plain reference-ordered array: the sub-range writes its coefficients at n
+        if (int rc = pd_xmask_coeffs_device(N, diag + 2 * q * xc * dim, q * xc, xc, 0, runs, path, s))
+            return rc;
+        PD_CUDA(cudaEventRecord(ctx->block_done[q], s));
+        PD_CUDA(cudaStreamWaitEvent(ctx->d2h, ctx->block_done[q], 0));
+        for (unsigned r = 0; r < (1u << kBits); ++r) {
+            const uint64_t off = 2 * pd_run_offset(N, kBits, q, r);
+            PD_CUDA(cudaMemcpyAsync(out + off, dout + off, run * sizeof(double2),
+                                    cudaMemcpyDeviceToHost, ctx->d2h));
+        }
+    }
+    PD_CUDA(cudaStreamSynchronize(ctx->d2h));
     PD_CUDA(cudaStreamSynchronize(ctx->stream));
+    PD_CUDA(cudaStreamSynchronize(ctx->stream2));
     return PD_OK;
 }
 

@@ -232,13 +232,15 @@ template <int K>
 static cudaError_t launch_gray(const double2* diag, unsigned N, uint64_t x0, uint64_t x_count,
                                unsigned run_bits, const RunOut& runs, cudaStream_t stream) {
     const K2Geometry g = k2_geometry(N, K, x_count);
-    static bool attr_set = false;  // per instantiation
-    if (!attr_set) {
+    static std::atomic<uint64_t> attr_set{0};  // per instantiation, one bit per device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!(attr_set.load() >> dev & 1)) {
         cudaError_t e = cudaFuncSetAttribute(gray_xmask_kernel<K>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              kK2MaxSmem);
         if (e != cudaSuccess) return e;
-        attr_set = true;
+        attr_set.fetch_or(1ull << dev);
     }
     const double scale = 1.0 / static_cast<double>(1ull << N);
     gray_xmask_kernel<K><<<static_cast<unsigned>(g.grid), kK2Threads, g.smem_bytes, stream>>>(

@@ -121,12 +121,14 @@ static cudaError_t wht_passes(double2* buf, unsigned N, uint64_t x0, uint64_t x_
     const unsigned R = N - L;
     if (R > 4) return cudaErrorInvalidValue;  // N <= 16
     const double scale = 1.0 / static_cast<double>(1ull << N);
-    static bool attr_set = false;
-    if (!attr_set) {
+    static std::atomic<uint64_t> attr_set{0};  // one bit per device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!(attr_set.load() >> dev & 1)) {
         cudaError_t e = cudaFuncSetAttribute(wht_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(sizeof(double2) << kWhtMaxL));
         if (e != cudaSuccess) return e;
-        attr_set = true;
+        attr_set.fetch_or(1ull << dev);
     }
     const uint64_t grid1 = x_count << R;
     wht_rows_kernel<<<static_cast<unsigned>(grid1), kWhtThreads, sizeof(double2) << L, stream>>>(
