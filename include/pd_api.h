@@ -121,6 +121,15 @@ PD_EXPORT int pd_diag_gather_device(unsigned num_qubits, const double* g, uint64
 PD_EXPORT int pd_xmask_coeffs_device(unsigned num_qubits, const double* diag, uint64_t x0, uint64_t x_count,
                            unsigned run_bits, double* const* run_out, pd_path path, void* stream);
 
+/* Every coefficient whose X-mask lies in [x0, x0 + x_count), straight from the matrix g,
+ * with the run addressing of pd_xmask_coeffs_device. GRAY: K1 into scratch, then K2.
+ * WHT: the fused two-pass transform (pass 1 gathers and butterflies the low 7 index bits
+ * into scratch, pass 2 the high bits) when N in [8,16] and x_count >= 32, else K1 + K4.
+ * scratch >= pd_scratch_bytes(N, x_count, path). This is one X-mask shard's work. */
+PD_EXPORT int pd_shard_coeffs_device(unsigned num_qubits, const double* g, uint64_t x0,
+                                     uint64_t x_count, unsigned run_bits, double* const* run_out,
+                                     void* scratch, pd_path path, void* stream);
+
 /* Global offset (in coefficients) of run r of X-mask shard g for p = run_bits. */
 PD_EXPORT uint64_t pd_run_offset(unsigned num_qubits, unsigned run_bits, uint64_t shard, uint64_t run);
 

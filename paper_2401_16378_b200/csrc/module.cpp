@@ -207,6 +207,18 @@ PYBIND11_MODULE(_paulidecomp, m) {
                                      path_of(path), P<void>(stream)));
     }, py::arg("num_qubits"), py::arg("diag"), py::arg("x0"), py::arg("x_count"),
           py::arg("run_bits"), py::arg("runs"), py::arg("path") = "gray", py::arg("stream") = 0);
+    d.def("shard_coeffs", [](unsigned N, std::uintptr_t g, std::uint64_t x0, std::uint64_t x_count,
+                             unsigned run_bits, const std::vector<std::uintptr_t>& runs,
+                             std::uintptr_t scratch, const std::string& path, std::uintptr_t stream) {
+        if (runs.size() != (std::size_t{1} << run_bits))
+            throw std::invalid_argument("need 2**run_bits run pointers");
+        std::vector<double*> rp(runs.size());
+        for (std::size_t r = 0; r < runs.size(); ++r) rp[r] = P<double>(runs[r]);
+        check(pd_shard_coeffs_device(N, P<const double>(g), x0, x_count, run_bits, rp.data(),
+                                     P<void>(scratch), path_of(path), P<void>(stream)));
+    }, py::arg("num_qubits"), py::arg("g"), py::arg("x0"), py::arg("x_count"), py::arg("run_bits"),
+          py::arg("runs"), py::arg("scratch"), py::arg("path") = "gray", py::arg("stream") = 0,
+          "All coefficients of an X-mask range straight from G (one shard's work).");
     d.def("coeff_batch", [](unsigned N, std::uintptr_t g, std::uintptr_t ns, std::uint64_t count,
                             bool slow, std::uintptr_t out, std::uintptr_t stream) {
         check(pd_coeff_batch_device(N, P<const double>(g), P<const std::uint64_t>(ns), count,

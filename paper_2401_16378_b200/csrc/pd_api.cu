@@ -249,6 +249,37 @@ int pd_xmask_coeffs_device(unsigned N, const double* diag, uint64_t x0, uint64_t
     return PD_OK;
 }
 
+int pd_shard_coeffs_device(unsigned N, const double* g, uint64_t x0, uint64_t x_count,
+                           unsigned run_bits, double* const* run_out, void* scratch, pd_path path,
+                           void* stream) {
+    if (int rc = check_qubits(N)) return rc;
+    if (int rc = check_device()) return rc;
+    if (!g || !scratch) return fail(PD_EINVAL, "null buffer");
+    if (path == PD_PATH_WHT && pdb::wht_fused_ok(N, x_count)) {
+        if (run_bits > pdb::kMaxRunBits || run_bits > N)
+            return fail(PD_EINVAL, "run_bits must be <= min(3, N)");
+        if (x_count == 0 || (x_count & (x_count - 1)) || x0 % x_count || x0 + x_count > (1ull << N) ||
+            x_count > (1ull << (N - run_bits)))
+            return fail(PD_EINVAL, "X-mask range must be an aligned power-of-two block of one shard");
+        double2* runs[pdb::kMaxRuns] = {};
+        for (unsigned r = 0; r < (1u << run_bits); ++r) {
+            if (!run_out || !run_out[r]) return fail(PD_EINVAL, "null run_out[%u]", r);
+            runs[r] = reinterpret_cast<double2*>(run_out[r]);
+        }
+        cudaError_t e = pdb::launch_wht_from_matrix(reinterpret_cast<const double2*>(g), N, x0,
+                                                    x_count, static_cast<double2*>(scratch),
+                                                    run_bits, runs, static_cast<cudaStream_t>(stream));
+        if (e != cudaSuccess) return cuda_fail(e, "fused WHT launch");
+        return PD_OK;
+    }
+    if (path != PD_PATH_GRAY && path != PD_PATH_WHT)
+        return fail(PD_EINVAL, "path must be PD_PATH_GRAY or PD_PATH_WHT");
+    if (int rc = pd_diag_gather_device(N, g, x0, x_count, static_cast<double*>(scratch), stream))
+        return rc;
+    return pd_xmask_coeffs_device(N, static_cast<const double*>(scratch), x0, x_count, run_bits,
+                                  run_out, path, stream);
+}
+
 int pd_decompose_device(unsigned N, const double* g, double* out, void* scratch, pd_path path,
                         void* stream) {
     if (int rc = check_qubits(N)) return rc;
@@ -262,11 +293,8 @@ int pd_decompose_device(unsigned N, const double* g, double* out, void* scratch,
     }
     if (path != PD_PATH_GRAY && path != PD_PATH_WHT) return fail(PD_EINVAL, "unknown path");
     if (!scratch) return fail(PD_EINVAL, "null scratch");
-    const uint64_t dim = 1ull << N;
-    if (int rc = pd_diag_gather_device(N, g, 0, dim, static_cast<double*>(scratch), stream)) return rc;
     double* runs[1] = {out};
-    return pd_xmask_coeffs_device(N, static_cast<const double*>(scratch), 0, dim, 0, runs, path,
-                                  stream);
+    return pd_shard_coeffs_device(N, g, 0, 1ull << N, 0, runs, scratch, path, stream);
 }
 
 int pd_coeff_batch_device(unsigned N, const double* g, const uint64_t* ns, uint64_t count, int slow,
@@ -332,8 +360,10 @@ int pd_decompose(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_path 
     // later blocks compute, so only the last block's D2H is exposed.
     double* dout = static_cast<double*>(ctx->out);
     double* diag = static_cast<double*>(ctx->scratch);
-    if (int rc = pd_diag_gather_device(N, static_cast<const double*>(ctx->g), 0, dim, diag, ctx->stream))
-        return rc;
+    const bool gray = path == PD_PATH_GRAY;
+    if (gray &&
+        pd_diag_gather_device(N, static_cast<const double*>(ctx->g), 0, dim, diag, ctx->stream))
+        return PD_ECUDA;
     PD_CUDA(cudaEventRecord(ctx->gathered, ctx->stream));
     PD_CUDA(cudaStreamWaitEvent(ctx->stream2, ctx->gathered, 0));
     constexpr unsigned kBits = 3;
@@ -343,8 +373,11 @@ int pd_decompose(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_path 
     for (unsigned q = 0; q < (1u << kBits); ++q) {
         cudaStream_t s = (q & 1) ? ctx->stream2 : ctx->stream;
         // the plain reference-ordered array: the sub-range writes its coefficients at n
-        if (int rc = pd_xmask_coeffs_device(N, diag + 2 * q * xc * dim, q * xc, xc, 0, runs, path, s))
-            return rc;
+        // WHT: each block gathers and transforms its own X-masks from G (fused two-pass)
+        const int rc = gray ? pd_xmask_coeffs_device(N, diag + 2 * q * xc * dim, q * xc, xc, 0, runs, path, s)
+                            : pd_shard_coeffs_device(N, static_cast<const double*>(ctx->g), q * xc, xc,
+                                                     0, runs, diag + 2 * q * xc * dim, path, s);
+        if (rc) return rc;
         PD_CUDA(cudaEventRecord(ctx->block_done[q], s));
         PD_CUDA(cudaStreamWaitEvent(ctx->d2h, ctx->block_done[q], 0));
         for (unsigned r = 0; r < (1u << kBits); ++r) {

@@ -26,6 +26,13 @@ uint64_t gray_xmask_grid(unsigned N, uint64_t x_count);
 cudaError_t launch_wht_xmask(const double2* diag, unsigned N, uint64_t x0, uint64_t x_count,
                              unsigned run_bits, double2* const* run_out, cudaStream_t stream);
 
+// K4 fused two-pass WHT straight from G for X-masks [x0, x0 + x_count) (N in [8,16],
+// x_count >= 32); scratch holds x_count * 2^N complex128 (the half-transformed diagonals)
+bool wht_fused_ok(unsigned N, uint64_t x_count);
+cudaError_t launch_wht_from_matrix(const double2* G, unsigned N, uint64_t x0, uint64_t x_count,
+                                   double2* scratch, unsigned run_bits, double2* const* run_out,
+                                   cudaStream_t stream);
+
 // in-place unnormalised Walsh-Hadamard transform of x_count rows of 2^N (N <= 16)
 cudaError_t launch_wht_inplace(double2* rows, unsigned N, uint64_t x_count, cudaStream_t stream);
 

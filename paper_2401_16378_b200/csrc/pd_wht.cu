@@ -111,6 +111,124 @@ __global__ void __launch_bounds__(kWhtThreads)
                     scale);
 }
 
+// ---------------------------------------------------------------------------------------
+// Fused two-pass WHT path (N >= 8): HBM traffic = read G + write D' + read D' + write out.
+//
+//   pass 1 (wht_gather_lo_kernel): CTA = 32 X-masks (one tile row block x_h) x 128 columns
+//     (4 column blocks C). Tile (R = C ^ x_h, C) of G holds D_x[C*32 + c] at (r, c) with
+//     x = x_h*32 + (r ^ c) (the K1 transposition), so the 4 coalesced tile loads yield 32
+//     diagonal segments of 128; the low 7 index bits are butterflied in shared memory and
+//     the segments are written to D' (coalesced 2 KiB rows).
+//   pass 2 (wht_hi_out_kernel): CTA = XPC X-masks x 8 adjacent low indices; loads 2^(N-7)
+//     128 B pieces per X-mask, butterflies the high N-7 bits, applies (-i)^{|x&z|} 2^-N and
+//     writes the coefficients: a warp covers (2 low x bits) x (3 low z bits), i.e. two
+//     contiguous 256 B runs of the reference-ordered array.
+//
+// Shared memory rows are padded by one element every 16 (pad(i) = i + i/16) so that both the
+// strided butterfly rounds and the XOR-permuted tile stores are bank-conflict free.
+
+constexpr unsigned kLoBits = 7;  // index bits done in pass 1
+
+__device__ __forceinline__ unsigned pad16(unsigned i) { return i + (i >> 4); }
+
+template <int RB>
+__device__ __forceinline__ void wht_round(double2* s, unsigned L, unsigned row_stride, unsigned rows,
+                                          unsigned b) {
+    const unsigned groups_log = L - RB;
+    const unsigned total = rows << groups_log;
+    for (unsigned g = threadIdx.x; g < total; g += blockDim.x) {
+        const unsigned row = g >> groups_log, rest = g & ((1u << groups_log) - 1);
+        const unsigned lo = rest & ((1u << b) - 1), hi = rest >> b;
+        const unsigned base = (hi << (b + RB)) | lo;
+        double2* r = s + row * row_stride;
+        double2 v[1 << RB];
+#pragma unroll
+        for (int k = 0; k < (1 << RB); ++k) v[k] = r[pad16(base + (static_cast<unsigned>(k) << b))];
+#pragma unroll
+        for (int h = 1; h < (1 << RB); h <<= 1) {
+#pragma unroll
+            for (int k = 0; k < (1 << RB); ++k) {
+                if (k & h) continue;
+                const double2 a = v[k], c = v[k + h];
+                v[k] = make_double2(a.x + c.x, a.y + c.y);
+                v[k + h] = make_double2(a.x - c.x, a.y - c.y);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < (1 << RB); ++k) r[pad16(base + (static_cast<unsigned>(k) << b))] = v[k];
+    }
+}
+
+// in-place WHT over index bits [b0, b0 + nb) of `rows` padded rows of 2^L elements
+__device__ void smem_wht(double2* s, unsigned L, unsigned row_stride, unsigned rows, unsigned b0,
+                         unsigned nb) {
+    for (unsigned b = b0; b < b0 + nb; b += 4) {
+        switch (b0 + nb - b >= 4 ? 4 : b0 + nb - b) {
+            case 4: wht_round<4>(s, L, row_stride, rows, b); break;
+            case 3: wht_round<3>(s, L, row_stride, rows, b); break;
+            case 2: wht_round<2>(s, L, row_stride, rows, b); break;
+            default: wht_round<1>(s, L, row_stride, rows, b); break;
+        }
+        __syncthreads();
+    }
+}
+
+constexpr unsigned kP1Row = (1u << kLoBits) + ((1u << kLoBits) >> 4);  // 136 padded elements
+constexpr size_t kP1Smem = 32 * kP1Row * sizeof(double2);                // 69,632 B
+
+__global__ void __launch_bounds__(kWhtThreads)
+    wht_gather_lo_kernel(const double2* __restrict__ G, unsigned N, uint64_t x0,
+                         double2* __restrict__ dprime) {
+    extern __shared__ __align__(16) double2 s1[];
+    const uint64_t dim = 1ull << N;
+    const unsigned groups_log = N - kLoBits;                  // 128-column groups per row
+    const uint64_t grp = blockIdx.x & ((1u << groups_log) - 1);
+    const uint64_t xb = blockIdx.x >> groups_log;             // local block of 32 X-masks
+    const uint64_t xh = (x0 >> 5) + xb;
+    for (unsigned e = threadIdx.x; e < 4 * 1024; e += kWhtThreads) {
+        const unsigned cb = e >> 10, r = (e >> 5) & 31, c = e & 31;
+        const uint64_t C = grp * 4 + cb, R = C ^ xh;
+        const double2 v = __ldcs(&G[((R << 5) + r) * dim + (C << 5) + c]);
+        s1[(r ^ c) * kP1Row + pad16(cb * 32 + c)] = v;
+    }
+    __syncthreads();
+    smem_wht(s1, kLoBits, kP1Row, 32, 0, kLoBits);
+    for (unsigned e = threadIdx.x; e < 32 * 128; e += kWhtThreads) {
+        const unsigned row = e >> 7, il = e & 127;
+        dprime[((xb << 5) + row) * dim + (grp << kLoBits) + il] = s1[row * kP1Row + pad16(il)];
+    }
+}
+
+__global__ void __launch_bounds__(kWhtThreads)
+    wht_hi_out_kernel(const double2* __restrict__ dprime, unsigned N, uint64_t x0,
+                      unsigned xpc_log, unsigned run_bits, Runs runs, double scale) {
+    extern __shared__ __align__(16) double2 s2[];
+    const uint64_t dim = 1ull << N;
+    const unsigned hb = N - kLoBits;                          // high bits done here
+    const unsigned L = hb + 3;                                // row = (hi, j), j = 3 low bits
+    const unsigned row_stride = (1u << L) + ((1u << L) >> 4);
+    const unsigned jblocks_log = kLoBits - 3;                 // 16 blocks of 8 low indices
+    const uint64_t jb = blockIdx.x & ((1u << jblocks_log) - 1);
+    const uint64_t xq = blockIdx.x >> jblocks_log;            // local group of 2^xpc_log X-masks
+    const unsigned xpc = 1u << xpc_log;
+    const unsigned total = xpc << L;
+    for (unsigned e = threadIdx.x; e < total; e += kWhtThreads) {
+        const unsigned xl = e >> L, hi = (e >> 3) & ((1u << hb) - 1), j = e & 7;
+        s2[xl * row_stride + pad16((hi << 3) | j)] =
+            __ldcs(&dprime[((xq << xpc_log) + xl) * dim + (static_cast<uint64_t>(hi) << kLoBits) +
+                           (jb << 3) + j]);
+    }
+    __syncthreads();
+    smem_wht(s2, L, row_stride, xpc, 3, hb);
+    for (unsigned e = threadIdx.x; e < total; e += kWhtThreads) {
+        const unsigned j = e & 7, xl = (e >> 3) & (xpc - 1), hi = e >> (3 + xpc_log);
+        const double2 v = s2[xl * row_stride + pad16((hi << 3) | j)];
+        const uint64_t x = x0 + (xq << xpc_log) + xl;
+        const uint64_t z = (static_cast<uint64_t>(hi) << kLoBits) | (jb << 3) | j;
+        store_coeff(runs, N, run_bits, x, z, v.x, v.y, scale);
+    }
+}
+
 }  // namespace
 
 // shared driver: rows pass, then (N > 12) the column pass; emit != 0 writes
@@ -153,6 +271,43 @@ cudaError_t launch_wht_xmask(const double2* diag_c, unsigned N, uint64_t x0, uin
     Runs runs{};
     for (unsigned r = 0; r < (1u << run_bits); ++r) runs.ptr[r] = run_out[r];
     return wht_passes(const_cast<double2*>(diag_c), N, x0, x_count, run_bits, runs, 1, stream);
+}
+
+bool wht_fused_ok(unsigned N, uint64_t x_count) { return N >= 8 && N <= 16 && x_count >= 32; }
+
+cudaError_t launch_wht_from_matrix(const double2* G, unsigned N, uint64_t x0, uint64_t x_count,
+                                   double2* scratch, unsigned run_bits, double2* const* run_out,
+                                   cudaStream_t stream) {
+    Runs runs{};
+    for (unsigned r = 0; r < (1u << run_bits); ++r) runs.ptr[r] = run_out[r];
+    static std::atomic<uint64_t> attr_set{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!(attr_set.load() >> dev & 1)) {
+        cudaError_t e = cudaFuncSetAttribute(wht_gather_lo_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kP1Smem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(wht_hi_out_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kP1Smem);
+        if (e != cudaSuccess) return e;
+        attr_set.fetch_or(1ull << dev);
+    }
+    const uint64_t grid1 = (x_count >> 5) << (N - kLoBits);
+    wht_gather_lo_kernel<<<static_cast<unsigned>(grid1), kWhtThreads, kP1Smem, stream>>>(G, N, x0, scratch);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const unsigned hb = N - kLoBits;
+    unsigned xpc_log = hb <= 6 ? 2 : (hb == 7 ? 2 : (hb == 8 ? 1 : 0));  // <= 4096 elements
+    while ((1ull << xpc_log) > x_count) --xpc_log;
+    const unsigned L = hb + 3;
+    const size_t smem = (sizeof(double2) << xpc_log) * ((1u << L) + ((1u << L) >> 4));
+    const uint64_t grid2 = (x_count >> xpc_log) << (kLoBits - 3);
+    const double scale = 1.0 / static_cast<double>(1ull << N);
+    wht_hi_out_kernel<<<static_cast<unsigned>(grid2), kWhtThreads, smem, stream>>>(
+        scratch, N, x0, xpc_log, run_bits, runs, scale);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_wht_inplace(double2* rows, unsigned N, uint64_t x_count, cudaStream_t stream) {

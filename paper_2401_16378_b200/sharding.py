@@ -62,14 +62,14 @@ class ShardPlan:
 
 
 def device_compute(path: str = "gray") -> ShardCompute:
-    """K1 + K2 (or K4) on the current CUDA stream."""
+    """One shard's coefficients straight from G on the current CUDA stream:
+    K1 + K2 (gray) or the fused two-pass WHT (wht), via pd_shard_coeffs_device."""
 
     def compute(G, x0, x_count, run_bits, runs, diag):
         N = int(G.shape[0]).bit_length() - 1
         stream = torch.cuda.current_stream(G.device).cuda_stream
-        _ext.device.diag_gather(N, G.data_ptr(), x0, x_count, diag.data_ptr(), stream)
-        _ext.device.xmask_coeffs(N, diag.data_ptr(), x0, x_count, run_bits,
-                                 [r.data_ptr() for r in runs], path, stream)
+        _ext.device.shard_coeffs(N, G.data_ptr(), x0, x_count, run_bits,
+                                 [r.data_ptr() for r in runs], diag.data_ptr(), path, stream)
 
     return compute
 

@@ -110,6 +110,15 @@ def test_full_n12_config4_sampled_bit_exact(pd, cuda, port):
     assert rel_err(pd.decompose(g, path="wht"), got) <= TOL
 
 
+@pytest.mark.parametrize("nq", [7, 8, 9, 10, 11, 13])
+def test_wht_fused_sizes(pd, cuda, port, nq):
+    g = normal_matrix(np.random.default_rng(700 + nq), nq)
+    got = pd.decompose(g, path="wht")
+    ns = np.random.default_rng(nq).integers(0, 4**nq, 4096).astype(np.uint64)
+    assert rel_err(got[ns.astype(np.int64)], port.coeff_batch(g, ns)) <= TOL
+    assert same_values(pd.decompose(g)[ns.astype(np.int64)], port.coeff_batch(g, ns))
+
+
 def test_integer_inputs_bit_exact_any_order(pd, cuda, port):
     # Gaussian-integer entries: every partial sum is exact, so all paths must agree bit for bit
     rng = np.random.default_rng(6)
@@ -155,6 +164,18 @@ def test_sharded_runs_assemble_full_array(pd, cuda):
             pd.device.xmask_coeffs(nq, diag.data_ptr(), shard * xc, xc, p, runs, "gray", 0)
         torch.cuda.synchronize()
         assert torch.equal(out, full), p
+        # the one-call shard entry point, both paths (WHT: fused two-pass from G)
+        for path in ("gray", "wht"):
+            out2 = torch.zeros_like(full)
+            for shard in range(2**p):
+                runs = [out2[pd.device.run_offset(nq, p, shard, r):].data_ptr() for r in range(2**p)]
+                pd.device.shard_coeffs(nq, g.data_ptr(), shard * xc, xc, p, runs, diag.data_ptr(), path, 0)
+            torch.cuda.synchronize()
+            if path == "gray":
+                assert torch.equal(out2, full), (p, path)
+            else:
+                err = float(torch.max(torch.abs(out2 - full)) / torch.max(torch.abs(full)))
+                assert err <= TOL, (p, err)
 
 
 def test_n14_config5(pd, cuda, port, golden):
