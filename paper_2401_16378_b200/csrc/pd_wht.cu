@@ -176,7 +176,7 @@ __device__ void smem_wht(double2* s, unsigned L, unsigned row_stride, unsigned r
 constexpr unsigned kP1Row = (1u << kLoBits) + ((1u << kLoBits) >> 4);  // 136 padded elements
 constexpr size_t kP1Smem = 32 * kP1Row * sizeof(double2);                // 69,632 B
 
-__global__ void __launch_bounds__(kWhtThreads)
+__global__ void __launch_bounds__(kWhtThreads, 2)
     wht_gather_lo_kernel(const double2* __restrict__ G, unsigned N, uint64_t x0,
                          double2* __restrict__ dprime) {
     extern __shared__ __align__(16) double2 s1[];
@@ -185,47 +185,97 @@ __global__ void __launch_bounds__(kWhtThreads)
     const uint64_t grp = blockIdx.x & ((1u << groups_log) - 1);
     const uint64_t xb = blockIdx.x >> groups_log;             // local block of 32 X-masks
     const uint64_t xh = (x0 >> 5) + xb;
-    for (unsigned e = threadIdx.x; e < 4 * 1024; e += kWhtThreads) {
+    constexpr int kIters = 4 * 1024 / kWhtThreads;            // 16 loads in flight per thread
+    double2 v[kIters];
+#pragma unroll
+    for (int it = 0; it < kIters; ++it) {
+        const unsigned e = threadIdx.x + it * kWhtThreads;
         const unsigned cb = e >> 10, r = (e >> 5) & 31, c = e & 31;
         const uint64_t C = grp * 4 + cb, R = C ^ xh;
-        const double2 v = __ldcs(&G[((R << 5) + r) * dim + (C << 5) + c]);
-        s1[(r ^ c) * kP1Row + pad16(cb * 32 + c)] = v;
+        v[it] = __ldcs(&G[((R << 5) + r) * dim + (C << 5) + c]);
+    }
+#pragma unroll
+    for (int it = 0; it < kIters; ++it) {
+        const unsigned e = threadIdx.x + it * kWhtThreads;
+        const unsigned cb = e >> 10, r = (e >> 5) & 31, c = e & 31;
+        s1[(r ^ c) * kP1Row + pad16(cb * 32 + c)] = v[it];
     }
     __syncthreads();
-    smem_wht(s1, kLoBits, kP1Row, 32, 0, kLoBits);
-    for (unsigned e = threadIdx.x; e < 32 * 128; e += kWhtThreads) {
+    wht_round<4>(s1, kLoBits, kP1Row, 32, 3);
+    __syncthreads();
+    wht_round<3>(s1, kLoBits, kP1Row, 32, 0);
+    __syncthreads();
+#pragma unroll
+    for (int it = 0; it < kIters; ++it) {
+        const unsigned e = threadIdx.x + it * kWhtThreads;
         const unsigned row = e >> 7, il = e & 127;
-        dprime[((xb << 5) + row) * dim + (grp << kLoBits) + il] = s1[row * kP1Row + pad16(il)];
+        __stcs(&dprime[((xb << 5) + row) * dim + (grp << kLoBits) + il], s1[row * kP1Row + pad16(il)]);
     }
 }
 
-__global__ void __launch_bounds__(kWhtThreads)
+// HB = N - 7 high index bits; XPC_LOG: X-masks per CTA (<= 4096 elements per CTA)
+template <int HB, int XPC_LOG>
+__global__ void __launch_bounds__(kWhtThreads, 2)
     wht_hi_out_kernel(const double2* __restrict__ dprime, unsigned N, uint64_t x0,
-                      unsigned xpc_log, unsigned run_bits, Runs runs, double scale) {
+                      unsigned run_bits, Runs runs, double scale) {
     extern __shared__ __align__(16) double2 s2[];
+    constexpr unsigned L = HB + 3;                            // row = (hi, j), j = 3 low bits
+    constexpr unsigned kRow = (1u << L) + ((1u << L) >> 4);
+    constexpr unsigned kTotal = (1u << XPC_LOG) << L;
+    constexpr int kIters = kTotal >= kWhtThreads ? kTotal / kWhtThreads : 1;
     const uint64_t dim = 1ull << N;
-    const unsigned hb = N - kLoBits;                          // high bits done here
-    const unsigned L = hb + 3;                                // row = (hi, j), j = 3 low bits
-    const unsigned row_stride = (1u << L) + ((1u << L) >> 4);
-    const unsigned jblocks_log = kLoBits - 3;                 // 16 blocks of 8 low indices
-    const uint64_t jb = blockIdx.x & ((1u << jblocks_log) - 1);
-    const uint64_t xq = blockIdx.x >> jblocks_log;            // local group of 2^xpc_log X-masks
-    const unsigned xpc = 1u << xpc_log;
-    const unsigned total = xpc << L;
-    for (unsigned e = threadIdx.x; e < total; e += kWhtThreads) {
-        const unsigned xl = e >> L, hi = (e >> 3) & ((1u << hb) - 1), j = e & 7;
-        s2[xl * row_stride + pad16((hi << 3) | j)] =
-            __ldcs(&dprime[((xq << xpc_log) + xl) * dim + (static_cast<uint64_t>(hi) << kLoBits) +
-                           (jb << 3) + j]);
+    constexpr unsigned kJBlocksLog = kLoBits - 3;             // 16 blocks of 8 low indices
+    const uint64_t jb = blockIdx.x & ((1u << kJBlocksLog) - 1);
+    const uint64_t xq = blockIdx.x >> kJBlocksLog;            // local group of X-masks
+    double2 v[kIters];
+#pragma unroll
+    for (int it = 0; it < kIters; ++it) {
+        const unsigned e = threadIdx.x + it * kWhtThreads;
+        if (e < kTotal) {
+            const unsigned xl = e >> L, hi = (e >> 3) & ((1u << HB) - 1), j = e & 7;
+            v[it] = __ldcs(&dprime[((xq << XPC_LOG) + xl) * dim +
+                                   (static_cast<uint64_t>(hi) << kLoBits) + (jb << 3) + j]);
+        }
+    }
+#pragma unroll
+    for (int it = 0; it < kIters; ++it) {
+        const unsigned e = threadIdx.x + it * kWhtThreads;
+        if (e < kTotal) {
+            const unsigned xl = e >> L, hi = (e >> 3) & ((1u << HB) - 1), j = e & 7;
+            s2[xl * kRow + pad16((hi << 3) | j)] = v[it];
+        }
     }
     __syncthreads();
-    smem_wht(s2, L, row_stride, xpc, 3, hb);
-    for (unsigned e = threadIdx.x; e < total; e += kWhtThreads) {
-        const unsigned j = e & 7, xl = (e >> 3) & (xpc - 1), hi = e >> (3 + xpc_log);
-        const double2 v = s2[xl * row_stride + pad16((hi << 3) | j)];
-        const uint64_t x = x0 + (xq << xpc_log) + xl;
-        const uint64_t z = (static_cast<uint64_t>(hi) << kLoBits) | (jb << 3) | j;
-        store_coeff(runs, N, run_bits, x, z, v.x, v.y, scale);
+#pragma unroll
+    for (unsigned b = 3; b < 3 + HB; b += 4) {
+        constexpr unsigned kEnd = 3 + HB;
+        if (kEnd - b >= 4) wht_round<4>(s2, L, kRow, 1u << XPC_LOG, b);
+        else if (kEnd - b == 3) wht_round<3>(s2, L, kRow, 1u << XPC_LOG, b);
+        else if (kEnd - b == 2) wht_round<2>(s2, L, kRow, 1u << XPC_LOG, b);
+        else wht_round<1>(s2, L, kRow, 1u << XPC_LOG, b);
+        __syncthreads();
+    }
+    // per-thread constants of the output mapping: e = (hi, xl, j) with j fastest
+    const uint64_t zlow = (jb << 3);
+    const unsigned low_bits = 2 * (N - run_bits);
+    const uint64_t low_mask = (low_bits >= 64) ? ~0ull : ((1ull << low_bits) - 1);
+#pragma unroll
+    for (int it = 0; it < kIters; ++it) {
+        const unsigned e = threadIdx.x + it * kWhtThreads;
+        if (e < kTotal) {
+            const unsigned j = e & 7, xl = (e >> 3) & ((1u << XPC_LOG) - 1), hi = e >> (3 + XPC_LOG);
+            const double2 w = s2[xl * kRow + pad16((hi << 3) | j)];
+            const uint64_t x = x0 + (xq << XPC_LOG) + xl;
+            const uint64_t z = (static_cast<uint64_t>(hi) << kLoBits) | zlow | j;
+            const unsigned ph = (3u * static_cast<unsigned>(__popcll(x & z))) & 3u;
+            const uint64_t n = tensor_number(x, z);
+            const unsigned run = static_cast<unsigned>(z >> (N - run_bits));
+            double2* p = runs.ptr[0];
+#pragma unroll
+            for (unsigned r = 1; r < kMaxRuns; ++r)
+                if (run == r) p = runs.ptr[r];
+            __stcs(&p[n & low_mask], apply_phase(ph, w.x, w.y, scale));
+        }
     }
 }
 
@@ -286,9 +336,6 @@ cudaError_t launch_wht_from_matrix(const double2* G, unsigned N, uint64_t x0, ui
     if (!(attr_set.load() >> dev & 1)) {
         cudaError_t e = cudaFuncSetAttribute(wht_gather_lo_kernel,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, kP1Smem);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(wht_hi_out_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     kP1Smem);
         if (e != cudaSuccess) return e;
         attr_set.fetch_or(1ull << dev);
     }
@@ -298,14 +345,33 @@ cudaError_t launch_wht_from_matrix(const double2* G, unsigned N, uint64_t x0, ui
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const unsigned hb = N - kLoBits;
-    unsigned xpc_log = hb <= 6 ? 2 : (hb == 7 ? 2 : (hb == 8 ? 1 : 0));  // <= 4096 elements
-    while ((1ull << xpc_log) > x_count) --xpc_log;
-    const unsigned L = hb + 3;
-    const size_t smem = (sizeof(double2) << xpc_log) * ((1u << L) + ((1u << L) >> 4));
-    const uint64_t grid2 = (x_count >> xpc_log) << (kLoBits - 3);
     const double scale = 1.0 / static_cast<double>(1ull << N);
-    wht_hi_out_kernel<<<static_cast<unsigned>(grid2), kWhtThreads, smem, stream>>>(
-        scratch, N, x0, xpc_log, run_bits, runs, scale);
+    // X-masks per CTA: 4 while 2^(hb+3) <= 1024, then 2, then 1 (<= 4096 elements, 68 KiB)
+    unsigned xpc_log = hb <= 7 ? 2 : (hb == 8 ? 1 : 0);
+    while ((1ull << xpc_log) > x_count) --xpc_log;
+    const size_t smem = (sizeof(double2) << xpc_log) * ((1u << (hb + 3)) + ((1u << (hb + 3)) >> 4));
+    const unsigned grid2 = static_cast<unsigned>((x_count >> xpc_log) << (kLoBits - 3));
+#define PD_HI(HBV, XL)                                                                        \
+    do {                                                                                      \
+        auto k = wht_hi_out_kernel<HBV, XL>;                                                  \
+        e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kP1Smem);    \
+        if (e == cudaSuccess)                                                                 \
+            k<<<grid2, kWhtThreads, smem, stream>>>(scratch, N, x0, run_bits, runs, scale);   \
+    } while (0)
+    switch (hb * 4 + xpc_log) {
+        case 1 * 4 + 2: PD_HI(1, 2); break;
+        case 2 * 4 + 2: PD_HI(2, 2); break;
+        case 3 * 4 + 2: PD_HI(3, 2); break;
+        case 4 * 4 + 2: PD_HI(4, 2); break;
+        case 5 * 4 + 2: PD_HI(5, 2); break;
+        case 6 * 4 + 2: PD_HI(6, 2); break;
+        case 7 * 4 + 2: PD_HI(7, 2); break;
+        case 8 * 4 + 1: PD_HI(8, 1); break;
+        case 9 * 4 + 0: PD_HI(9, 0); break;
+        default: return cudaErrorInvalidValue;
+    }
+#undef PD_HI
+    if (e != cudaSuccess) return e;
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return cudaGetLastError();
 }
