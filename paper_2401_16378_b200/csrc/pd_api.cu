@@ -97,9 +97,15 @@ struct pd_ctx {
     cudaStream_t stream = nullptr;   // H2D, K1, even X-mask blocks
     cudaStream_t stream2 = nullptr;  // odd X-mask blocks (overlaps the previous block's tail)
     cudaStream_t d2h = nullptr;      // coefficient download, overlapped with later blocks
+    cudaStream_t h2d = nullptr;      // column-segment upload + K1, overlapped with K2 segments
     static constexpr int kBlocks = 8;
+    static constexpr int kSegs = 4;
     cudaEvent_t gathered = nullptr;
     cudaEvent_t block_done[kBlocks] = {};
+    cudaEvent_t cols_ready[kSegs] = {};
+    cudaEvent_t seg_done = nullptr;
+    void* part = nullptr;            // raw partial sums between walk segments
+    size_t part_bytes = 0;
     void* g = nullptr;
     size_t g_bytes = 0;
     void* out = nullptr;
@@ -160,9 +166,13 @@ int pd_ctx_create(int device, pd_ctx** out) {
     cudaError_t e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->gathered, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->seg_done, cudaEventDisableTiming);
     for (int b = 0; e == cudaSuccess && b < pd_ctx::kBlocks; ++b)
         e = cudaEventCreateWithFlags(&ctx->block_done[b], cudaEventDisableTiming);
+    for (int b = 0; e == cudaSuccess && b < pd_ctx::kSegs; ++b)
+        e = cudaEventCreateWithFlags(&ctx->cols_ready[b], cudaEventDisableTiming);
     if (e != cudaSuccess) {
         pd_ctx_destroy(ctx);
         return cuda_fail(e, "cudaStreamCreate");
@@ -174,14 +184,17 @@ int pd_ctx_create(int device, pd_ctx** out) {
 int pd_ctx_destroy(pd_ctx* ctx) {
     if (!ctx) return PD_OK;
     cudaSetDevice(ctx->device);
-    for (cudaStream_t s : {ctx->stream, ctx->stream2, ctx->d2h})
+    for (cudaStream_t s : {ctx->stream, ctx->stream2, ctx->d2h, ctx->h2d})
         if (s) cudaStreamSynchronize(s);
-    for (void* p : {ctx->g, ctx->out, ctx->scratch, ctx->ns})
+    for (void* p : {ctx->g, ctx->out, ctx->scratch, ctx->ns, ctx->part})
         if (p) cudaFree(p);
-    if (ctx->gathered) cudaEventDestroy(ctx->gathered);
+    for (cudaEvent_t ev : {ctx->gathered, ctx->seg_done})
+        if (ev) cudaEventDestroy(ev);
     for (cudaEvent_t ev : ctx->block_done)
         if (ev) cudaEventDestroy(ev);
-    for (cudaStream_t s : {ctx->stream, ctx->stream2, ctx->d2h})
+    for (cudaEvent_t ev : ctx->cols_ready)
+        if (ev) cudaEventDestroy(ev);
+    for (cudaStream_t s : {ctx->stream, ctx->stream2, ctx->d2h, ctx->h2d})
         if (s) cudaStreamDestroy(s);
     delete ctx;
     return PD_OK;
@@ -344,9 +357,9 @@ int pd_decompose(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_path 
     if (int rc = ctx->ensure(&ctx->out, &ctx->out_bytes, bytes)) return rc;
     const uint64_t sb = pd_scratch_bytes(N, 1ull << N, path);
     if (sb && (ctx->ensure(&ctx->scratch, &ctx->scratch_bytes, sb) != PD_OK)) return PD_ENOMEM;
-    if (int rc = upload(ctx, ctx->g, g, bytes)) return rc;
     const uint64_t dim = 1ull << N;
     if (path == PD_PATH_NAIVE || N < 10) {
+        if (int rc = upload(ctx, ctx->g, g, bytes)) return rc;
         if (int rc = pd_decompose_device(N, static_cast<const double*>(ctx->g),
                                          static_cast<double*>(ctx->out), ctx->scratch, path,
                                          ctx->stream))
@@ -355,28 +368,73 @@ int pd_decompose(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_path 
         PD_CUDA(cudaStreamSynchronize(ctx->stream));
         return PD_OK;
     }
-    // Pipelined: K1 over all X-masks, then K2 (or K4) in 8 X-mask blocks alternating over two
-    // streams; block q's coefficients (8 runs of 4^(N-3), pd_run_offset) are downloaded while
-    // later blocks compute, so only the last block's D2H is exposed.
+    // Pipelined host path.
+    //  * Upload. Gray path with >= 2 walk chunks (N >= 12): G goes up in column segments in
+    //    the Gray order of the walk (columns [gray(s) W, gray(s) W + W) are exactly the
+    //    diagonal indices visited by walk segment s), each followed by K1 on those columns,
+    //    while K2 runs the previous walk segment; K2 segments chain through raw partial sums,
+    //    so the result is bit-identical to one launch. Otherwise G goes up in one copy.
+    //  * Download. The last K2 segment (or the whole WHT) runs in 8 X-mask blocks alternating
+    //    over two streams; block q's coefficients (8 runs of 4^(N-3), pd_run_offset) are copied
+    //    back while later blocks compute, so only the last block's D2H is exposed.
     double* dout = static_cast<double*>(ctx->out);
     double* diag = static_cast<double*>(ctx->scratch);
+    double* gdev = static_cast<double*>(ctx->g);
     const bool gray = path == PD_PATH_GRAY;
-    if (gray &&
-        pd_diag_gather_device(N, static_cast<const double*>(ctx->g), 0, dim, diag, ctx->stream))
-        return PD_ECUDA;
-    PD_CUDA(cudaEventRecord(ctx->gathered, ctx->stream));
-    PD_CUDA(cudaStreamWaitEvent(ctx->stream2, ctx->gathered, 0));
+    const unsigned nch = gray ? pdb::gray_xmask_chunks(N) : 1;
+    const unsigned segs = nch >= 4 ? 4u : nch;
     constexpr unsigned kBits = 3;
     const uint64_t xc = dim >> kBits;
     const uint64_t run = 1ull << (2 * (N - kBits));
+    double2* part = nullptr;
+    unsigned c_last = 0;
+    if (gray && segs >= 2) {
+        if (int rc = ctx->ensure(&ctx->part, &ctx->part_bytes, bytes)) return rc;
+        part = static_cast<double2*>(ctx->part);
+        const uint64_t W = dim / segs;
+        for (unsigned sg = 0; sg < segs; ++sg) {
+            const uint64_t col0 = (sg ^ (sg >> 1)) * W;  // Gray order of the walk segments
+            PD_CUDA(cudaMemcpy2DAsync(gdev + 2 * col0, dim * sizeof(double2), g + 2 * col0,
+                                      dim * sizeof(double2), W * sizeof(double2), dim,
+                                      cudaMemcpyHostToDevice, ctx->h2d));
+            cudaError_t e = pdb::launch_diag_gather_cols(reinterpret_cast<const double2*>(gdev), N,
+                                                         0, dim, col0, W,
+                                                         reinterpret_cast<double2*>(diag), ctx->h2d);
+            if (e != cudaSuccess) return cuda_fail(e, "diag_gather launch");
+            PD_CUDA(cudaEventRecord(ctx->cols_ready[sg], ctx->h2d));
+        }
+        const unsigned per = nch / segs;
+        for (unsigned sg = 0; sg + 1 < segs; ++sg) {
+            PD_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->cols_ready[sg], 0));
+            cudaError_t e = pdb::launch_gray_segment(reinterpret_cast<const double2*>(diag), N, 0,
+                                                     dim, sg * per, (sg + 1) * per,
+                                                     sg ? part : nullptr, part, 0, nullptr,
+                                                     ctx->stream);
+            if (e != cudaSuccess) return cuda_fail(e, "gray segment launch");
+        }
+        c_last = (segs - 1) * per;
+        PD_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->cols_ready[segs - 1], 0));
+        PD_CUDA(cudaEventRecord(ctx->gathered, ctx->stream));
+    } else {
+        if (int rc = upload(ctx, ctx->g, g, bytes)) return rc;
+        if (gray && pd_diag_gather_device(N, gdev, 0, dim, diag, ctx->stream)) return PD_ECUDA;
+        PD_CUDA(cudaEventRecord(ctx->gathered, ctx->stream));
+    }
+    PD_CUDA(cudaStreamWaitEvent(ctx->stream2, ctx->gathered, 0));
     double* runs[1] = {dout};
     for (unsigned q = 0; q < (1u << kBits); ++q) {
         cudaStream_t s = (q & 1) ? ctx->stream2 : ctx->stream;
-        // the plain reference-ordered array: the sub-range writes its coefficients at n
-        // WHT: each block gathers and transforms its own X-masks from G (fused two-pass)
-        const int rc = gray ? pd_xmask_coeffs_device(N, diag + 2 * q * xc * dim, q * xc, xc, 0, runs, path, s)
-                            : pd_shard_coeffs_device(N, static_cast<const double*>(ctx->g), q * xc, xc,
-                                                     0, runs, diag + 2 * q * xc * dim, path, s);
+        int rc;
+        if (gray) {
+            double2* out_runs[1] = {reinterpret_cast<double2*>(dout)};
+            cudaError_t e = pdb::launch_gray_segment(
+                reinterpret_cast<const double2*>(diag) + q * xc * dim, N, q * xc, xc, c_last, 0,
+                part ? part + q * xc * dim : nullptr, nullptr, 0, out_runs, s);
+            rc = e == cudaSuccess ? PD_OK : cuda_fail(e, "gray block launch");
+        } else {
+            // WHT: each block gathers and transforms its own X-masks from G (fused two-pass)
+            rc = pd_shard_coeffs_device(N, gdev, q * xc, xc, 0, runs, diag + 2 * q * xc * dim, path, s);
+        }
         if (rc) return rc;
         PD_CUDA(cudaEventRecord(ctx->block_done[q], s));
         PD_CUDA(cudaStreamWaitEvent(ctx->d2h, ctx->block_done[q], 0));
@@ -389,6 +447,7 @@ int pd_decompose(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_path 
     PD_CUDA(cudaStreamSynchronize(ctx->d2h));
     PD_CUDA(cudaStreamSynchronize(ctx->stream));
     PD_CUDA(cudaStreamSynchronize(ctx->stream2));
+    PD_CUDA(cudaStreamSynchronize(ctx->h2d));
     return PD_OK;
 }
 

@@ -133,30 +133,48 @@ __device__ __forceinline__ void gray_block(const double2* __restrict__ blk, unsi
     }
 }
 
-template <int K>
-__global__ void __launch_bounds__(kK2Threads, 2)
-    gray_xmask_kernel(const double2* __restrict__ diag, unsigned N, uint64_t x0, uint64_t x_count,
-                      unsigned tpx_log, unsigned xc_log, unsigned cpx_log, unsigned ci_log,
-                      unsigned nchunks, unsigned run_bits, RunOut runs, double scale) {
+// Everything a K2 launch needs. A launch covers the walk steps of chunks [c_begin, c_end)
+// (chunk c = steps [c C, (c+1) C), i.e. diagonal indices [gray(c) C, gray(c) C + C)): it starts
+// from the raw sums in part_in (or zero) and ends by storing raw sums to part_out, or — when
+// part_out is null — the finished coefficients. Continuing a chain from stored sums keeps each
+// coefficient's summation order, so segmented launches are bit-identical to one launch.
+struct K2Params {
+    const double2* diag;       // rows of the X-masks [x0, x0 + x_count)
+    uint64_t x0, x_count;
+    unsigned N, tpx_log, xc_log, cpx_log, ci_log;
+    unsigned c_begin, c_end;
+    const double2* part_in;    // raw sums S[(x - x0) 2^N + z], or null
+    double2* part_out;         // raw sums out, or null for coefficients
+    unsigned run_bits;
+    RunOut runs;
+    double scale;
+};
+
+// SEG = false: the whole walk from zero to coefficients (c_begin = 0, no partial sums); kept
+// as a separate instantiation so the common case compiles without the segment logic.
+template <int K, bool SEG>
+__global__ void __launch_bounds__(kK2Threads, 2) gray_xmask_kernel(const K2Params P) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const unsigned tid = threadIdx.x;
+    const unsigned N = P.N, tpx_log = P.tpx_log, xc_log = P.xc_log, ci_log = P.ci_log;
     const uint64_t dim = 1ull << N;
     const unsigned C = 1u << ci_log;
     const uint64_t stage_elems = static_cast<uint64_t>(C) << xc_log;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);  // 2 mbarriers, then the stages
     double2* stage_buf = reinterpret_cast<double2*>(smem_raw + kK2BarBytes);
+    const double2* __restrict__ diag = P.diag;
 
     const uint64_t cta = blockIdx.x;
-    const uint64_t xblock = cta >> cpx_log;                    // which group of 2^xc_log x
-    const unsigned zpart = static_cast<unsigned>(cta & ((1u << cpx_log) - 1));
+    const uint64_t xblock = cta >> P.cpx_log;                  // which group of 2^xc_log x
+    const unsigned zpart = static_cast<unsigned>(cta & ((1u << P.cpx_log) - 1));
     const uint64_t xl_base = xblock << xc_log;                 // local x index of the CTA's first x
     const unsigned xl_cta = tid >> tpx_log;                    // x within CTA
     const uint64_t xl = xl_base + xl_cta;                      // local x (row of diag)
-    const bool active = xl < x_count;
-    const uint64_t x = x0 + xl;
+    const bool active = xl < P.x_count;
+    const uint64_t x = P.x0 + xl;
     const uint64_t zh = (static_cast<uint64_t>(zpart) << tpx_log) | (tid & ((1u << tpx_log) - 1));
-    const uint64_t rows_here = (x_count - xl_base) < (1ull << xc_log) ? (x_count - xl_base)
-                                                                      : (1ull << xc_log);
+    const uint64_t rows_here = (P.x_count - xl_base) < (1ull << xc_log) ? (P.x_count - xl_base)
+                                                                        : (1ull << xc_log);
 
     if (tid == 0) {
         mbar_init(&bars[0], 1);
@@ -179,27 +197,42 @@ __global__ void __launch_bounds__(kK2Threads, 2)
         }
     };
 
+    const unsigned c_begin = SEG ? P.c_begin : 0u;
+    const unsigned nseg = P.c_end - c_begin;
     if (tid == 0) {
-        issue(0, 0);
-        if (nchunks > 1) issue(1, 1);
+        issue(c_begin, 0);
+        if (nseg > 1) issue(c_begin + 1, 1);
     }
 
     double ar[1 << K], ai[1 << K];
+    if (SEG && P.part_in != nullptr && active) {
+        const double2* src = P.part_in + xl * dim + (zh << K);
 #pragma unroll
-    for (int j = 0; j < (1 << K); ++j) ar[j] = ai[j] = 0.0;
+        for (int j = 0; j < (1 << K); ++j) {
+            const double2 v = src[j];
+            ar[j] = v.x;
+            ai[j] = v.y;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < (1 << K); ++j) ar[j] = ai[j] = 0.0;
+    }
 
-    unsigned sgn = 0;  // (-1)^{|gray(kh) & zh|} as a sign-bit mask
     const unsigned blocks_per_chunk = C >> K;
     const uint32_t zh32 = static_cast<uint32_t>(zh);
+    const uint64_t kh_start = static_cast<uint64_t>(c_begin) * blocks_per_chunk;
+    // (-1)^{|gray(kh) & zh|} as a sign-bit mask: direct at the segment start, then the recurrence
+    unsigned sgn = SEG ? static_cast<unsigned>(__popcll(gray(kh_start) & zh) & 1) << 31 : 0u;
 
-    for (unsigned c = 0; c < nchunks; ++c) {
-        const unsigned s = c & 1u;
-        mbar_wait(&bars[s], (c >> 1) & 1u);
+    for (unsigned ci = 0; ci < nseg; ++ci) {
+        const unsigned c = c_begin + ci;
+        const unsigned s = ci & 1u;
+        mbar_wait(&bars[s], (ci >> 1) & 1u);
         const double2* base = stage_buf + s * stage_elems + static_cast<uint64_t>(xl_cta) * C;
         const uint64_t kh0 = static_cast<uint64_t>(c) * blocks_per_chunk;
         for (unsigned b = 0; b < blocks_per_chunk; b += 2) {
             const uint64_t kh = kh0 + b;
-            if (kh != 0) sgn ^= ((zh32 >> __ffsll(static_cast<long long>(kh)) - 1) & 1u) << 31;
+            if (kh != kh_start) sgn ^= ((zh32 >> __ffsll(static_cast<long long>(kh)) - 1) & 1u) << 31;
             const unsigned off = static_cast<unsigned>((gray(kh) << K) & (C - 1));
             gray_block<K, false>(base + off, sgn, ar, ai);
             if (b + 1 < blocks_per_chunk) {
@@ -209,57 +242,94 @@ __global__ void __launch_bounds__(kK2Threads, 2)
                 gray_block<K, true>(base + off1, sgn, ar, ai);
             }
         }
-        if (c + 2 < nchunks) {
+        if (ci + 2 < nseg) {
             __syncthreads();
             if (tid == 0) issue(c + 2, s);
         }
     }
 
     if (!active) return;
-    const unsigned low_bits = 2 * (N - run_bits);
+    if (SEG && P.part_out != nullptr) {
+        double2* dst = P.part_out + xl * dim + (zh << K);
+#pragma unroll
+        for (int j = 0; j < (1 << K); ++j) dst[j] = make_double2(ar[j], ai[j]);
+        return;
+    }
+    const unsigned low_bits = 2 * (N - P.run_bits);
     const uint64_t low_mask = (low_bits >= 64) ? ~0ull : ((1ull << low_bits) - 1);
 #pragma unroll
     for (int zl = 0; zl < (1 << K); ++zl) {
         const uint64_t z = (zh << K) | static_cast<uint64_t>(zl);
         const unsigned ph = (3u * static_cast<unsigned>(__popcll(x & z))) & 3u;
         const uint64_t n = tensor_number(x, z);
-        const unsigned run = static_cast<unsigned>(z >> (N - run_bits));
-        run_ptr(runs, run)[n & low_mask] = apply_phase(ph, ar[zl], ai[zl], scale);
+        const unsigned run = static_cast<unsigned>(z >> (N - P.run_bits));
+        run_ptr(P.runs, run)[n & low_mask] = apply_phase(ph, ar[zl], ai[zl], P.scale);
     }
 }
 
 template <int K>
-static cudaError_t launch_gray(const double2* diag, unsigned N, uint64_t x0, uint64_t x_count,
-                               unsigned run_bits, const RunOut& runs, cudaStream_t stream) {
-    const K2Geometry g = k2_geometry(N, K, x_count);
+static cudaError_t launch_gray(const K2Params& P0, unsigned run_bits, cudaStream_t stream) {
+    const K2Geometry g = k2_geometry(P0.N, K, P0.x_count);
     static std::atomic<uint64_t> attr_set{0};  // per instantiation, one bit per device
     int dev = 0;
     cudaGetDevice(&dev);
     if (!(attr_set.load() >> dev & 1)) {
-        cudaError_t e = cudaFuncSetAttribute(gray_xmask_kernel<K>,
+        cudaError_t e = cudaFuncSetAttribute(gray_xmask_kernel<K, false>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              kK2MaxSmem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(gray_xmask_kernel<K, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kK2MaxSmem);
         if (e != cudaSuccess) return e;
         attr_set.fetch_or(1ull << dev);
     }
-    const double scale = 1.0 / static_cast<double>(1ull << N);
-    gray_xmask_kernel<K><<<static_cast<unsigned>(g.grid), kK2Threads, g.smem_bytes, stream>>>(
-        diag, N, x0, x_count, g.tpx_log, g.xc_log, g.cpx_log, g.ci_log, g.nchunks, run_bits, runs,
-        scale);
+    K2Params P = P0;
+    P.tpx_log = g.tpx_log;
+    P.xc_log = g.xc_log;
+    P.cpx_log = g.cpx_log;
+    P.ci_log = g.ci_log;
+    if (P.c_end == 0 || P.c_end > g.nchunks) P.c_end = g.nchunks;
+    if (P.c_begin >= P.c_end) return cudaErrorInvalidValue;
+    P.run_bits = run_bits;
+    P.scale = 1.0 / static_cast<double>(1ull << P.N);
+    const bool seg = P.c_begin != 0 || P.c_end != g.nchunks || P.part_in || P.part_out;
+    if (seg)
+        gray_xmask_kernel<K, true><<<static_cast<unsigned>(g.grid), kK2Threads, g.smem_bytes, stream>>>(P);
+    else
+        gray_xmask_kernel<K, false><<<static_cast<unsigned>(g.grid), kK2Threads, g.smem_bytes, stream>>>(P);
     return count_launch();
+}
+
+cudaError_t launch_gray_segment(const double2* diag, unsigned N, uint64_t x0, uint64_t x_count,
+                                unsigned c_begin, unsigned c_end, const double2* part_in,
+                                double2* part_out, unsigned run_bits, double2* const* run_out,
+                                cudaStream_t stream) {
+    K2Params P{};
+    P.diag = diag;
+    P.x0 = x0;
+    P.x_count = x_count;
+    P.N = N;
+    P.c_begin = c_begin;
+    P.c_end = c_end;
+    P.part_in = part_in;
+    P.part_out = part_out;
+    if (run_out != nullptr)
+        for (unsigned r = 0; r < (1u << run_bits); ++r) P.runs.ptr[r] = run_out[r];
+    switch (N < 4 ? N : 4) {
+        case 1: return launch_gray<1>(P, run_bits, stream);
+        case 2: return launch_gray<2>(P, run_bits, stream);
+        case 3: return launch_gray<3>(P, run_bits, stream);
+        default: return launch_gray<4>(P, run_bits, stream);
+    }
 }
 
 cudaError_t launch_gray_xmask(const double2* diag, unsigned N, uint64_t x0, uint64_t x_count,
                               unsigned run_bits, double2* const* run_out, cudaStream_t stream) {
-    RunOut runs{};
-    for (unsigned r = 0; r < (1u << run_bits); ++r) runs.ptr[r] = run_out[r];
-    switch (N < 4 ? N : 4) {
-        case 1: return launch_gray<1>(diag, N, x0, x_count, run_bits, runs, stream);
-        case 2: return launch_gray<2>(diag, N, x0, x_count, run_bits, runs, stream);
-        case 3: return launch_gray<3>(diag, N, x0, x_count, run_bits, runs, stream);
-        default: return launch_gray<4>(diag, N, x0, x_count, run_bits, runs, stream);
-    }
+    return launch_gray_segment(diag, N, x0, x_count, 0, 0, nullptr, nullptr, run_bits, run_out,
+                               stream);
 }
+
+unsigned gray_xmask_chunks(unsigned N) { return k2_geometry(N, N < 4 ? N : 4, 1).nchunks; }
 
 uint64_t gray_xmask_grid(unsigned N, uint64_t x_count) {
     return k2_geometry(N, N < 4 ? N : 4, x_count).grid;
@@ -279,12 +349,12 @@ constexpr int kK1Threads = 256;
 
 __global__ void __launch_bounds__(kK1Threads)
     diag_gather_kernel(const double2* __restrict__ G, unsigned N, uint64_t x0, unsigned t_log,
-                       uint64_t col_blocks_log, double2* __restrict__ diag) {
+                       uint64_t col_blocks_log, uint64_t cb_begin, double2* __restrict__ diag) {
     __shared__ double2 tile[32 * 32];
     const unsigned T = 1u << t_log;
     const uint64_t dim = 1ull << N;
     const uint64_t bid = blockIdx.x;
-    const uint64_t cb = bid & ((1ull << col_blocks_log) - 1);
+    const uint64_t cb = cb_begin + (bid & ((1ull << col_blocks_log) - 1));
     const uint64_t xb = bid >> col_blocks_log;          // local x block
     const uint64_t xh = (x0 >> t_log) + xb;             // global x block
     const uint64_t rb = cb ^ xh;                        // row block
@@ -300,15 +370,20 @@ __global__ void __launch_bounds__(kK1Threads)
     }
 }
 
-cudaError_t launch_diag_gather(const double2* G, unsigned N, uint64_t x0, uint64_t x_count,
-                               double2* diag, cudaStream_t stream) {
+cudaError_t launch_diag_gather_cols(const double2* G, unsigned N, uint64_t x0, uint64_t x_count,
+                                    uint64_t col0, uint64_t cols, double2* diag, cudaStream_t stream) {
     unsigned t_log = N < 5 ? N : 5;
-    while ((1ull << t_log) > x_count) --t_log;  // x_count is a power of two
-    const uint64_t col_blocks_log = N - t_log;
+    while ((1ull << t_log) > x_count || (1ull << t_log) > cols) --t_log;  // powers of two
+    const uint64_t col_blocks_log = 63 - __builtin_clzll(cols >> t_log);
     const uint64_t grid = (x_count >> t_log) << col_blocks_log;
     diag_gather_kernel<<<static_cast<unsigned>(grid), kK1Threads, 0, stream>>>(
-        G, N, x0, t_log, col_blocks_log, diag);
+        G, N, x0, t_log, col_blocks_log, col0 >> t_log, diag);
     return count_launch();
+}
+
+cudaError_t launch_diag_gather(const double2* G, unsigned N, uint64_t x0, uint64_t x_count,
+                               double2* diag, cudaStream_t stream) {
+    return launch_diag_gather_cols(G, N, x0, x_count, 0, 1ull << N, diag, stream);
 }
 
 // ============================================================================

@@ -17,6 +17,18 @@ extern std::atomic<uint64_t> g_launches;
 cudaError_t launch_diag_gather(const double2* G, unsigned N, uint64_t x0, uint64_t x_count,
                                double2* diag, cudaStream_t stream);
 
+// K1 restricted to the columns [col0, col0 + cols) (a power-of-two aligned range)
+cudaError_t launch_diag_gather_cols(const double2* G, unsigned N, uint64_t x0, uint64_t x_count,
+                                    uint64_t col0, uint64_t cols, double2* diag, cudaStream_t stream);
+
+// K2 over the walk chunks [c_begin, c_end) (c_end = 0: to the end), continuing from raw sums
+// part_in (null: from zero) and storing raw sums to part_out (null: finished coefficients)
+cudaError_t launch_gray_segment(const double2* diag, unsigned N, uint64_t x0, uint64_t x_count,
+                                unsigned c_begin, unsigned c_end, const double2* part_in,
+                                double2* part_out, unsigned run_bits, double2* const* run_out,
+                                cudaStream_t stream);
+unsigned gray_xmask_chunks(unsigned N);  // walk chunks per diagonal (1 for N < 12)
+
 // K2: Gray-code sums for the X-masks [x0, x0 + x_count); run addressing as in pd_api.h
 cudaError_t launch_gray_xmask(const double2* diag, unsigned N, uint64_t x0, uint64_t x_count,
                               unsigned run_bits, double2* const* run_out, cudaStream_t stream);

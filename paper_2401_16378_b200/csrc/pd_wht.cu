@@ -159,20 +159,6 @@ __device__ __forceinline__ void wht_round(double2* s, unsigned L, unsigned row_s
     }
 }
 
-// in-place WHT over index bits [b0, b0 + nb) of `rows` padded rows of 2^L elements
-__device__ void smem_wht(double2* s, unsigned L, unsigned row_stride, unsigned rows, unsigned b0,
-                         unsigned nb) {
-    for (unsigned b = b0; b < b0 + nb; b += 4) {
-        switch (b0 + nb - b >= 4 ? 4 : b0 + nb - b) {
-            case 4: wht_round<4>(s, L, row_stride, rows, b); break;
-            case 3: wht_round<3>(s, L, row_stride, rows, b); break;
-            case 2: wht_round<2>(s, L, row_stride, rows, b); break;
-            default: wht_round<1>(s, L, row_stride, rows, b); break;
-        }
-        __syncthreads();
-    }
-}
-
 constexpr unsigned kP1Row = (1u << kLoBits) + ((1u << kLoBits) >> 4);  // 136 padded elements
 constexpr size_t kP1Smem = 32 * kP1Row * sizeof(double2);                // 69,632 B
 

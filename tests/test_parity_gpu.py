@@ -119,6 +119,18 @@ def test_wht_fused_sizes(pd, cuda, port, nq):
     assert same_values(pd.decompose(g)[ns.astype(np.int64)], port.coeff_batch(g, ns))
 
 
+@pytest.mark.parametrize("nq", [12, 13])
+def test_host_pipeline_matches_device_path(pd, cuda, nq):
+    import torch
+    g = normal_matrix(np.random.default_rng(1300 + nq), nq)
+    gd = torch.from_numpy(g).to(cuda)
+    out = torch.empty(4**nq, dtype=torch.complex128, device=cuda)
+    scratch = torch.empty(4**nq, dtype=torch.complex128, device=cuda)
+    pd.device.decompose(nq, gd.data_ptr(), out.data_ptr(), scratch.data_ptr(), "gray", 0)
+    torch.cuda.synchronize()
+    assert np.array_equal(pd.decompose(g), out.cpu().numpy())
+
+
 def test_integer_inputs_bit_exact_any_order(pd, cuda, port):
     # Gaussian-integer entries: every partial sum is exact, so all paths must agree bit for bit
     rng = np.random.default_rng(6)
@@ -204,6 +216,11 @@ def test_n14_config5(pd, cuda, port, golden):
     want = port.coeff_batch(gh, sample.astype(np.uint64))
     got = out[torch.from_numpy(sample).to(cuda)].cpu().numpy()
     assert same_values(got, want)
+    # the host-buffer path (segmented column upload + chained K2 segments + block D2H)
+    # must reproduce the device-resident result exactly
+    host = pd.decompose(gh)
+    assert np.array_equal(host, out.cpu().numpy())
+    del host
     fro = float(torch.sum(torch.abs(g) ** 2))
     par = float(2**nq * torch.sum(torch.abs(out) ** 2))
     assert abs(fro - par) <= 1e-10 * fro
