@@ -48,7 +48,8 @@ typedef enum pd_status {
     PD_ELENGTH = -2, /* std::length_error */
     PD_ENOMEM = -3,  /* std::bad_alloc / cudaErrorMemoryAllocation */
     PD_ECUDA = -4,   /* any other CUDA runtime failure */
-    PD_ENODEV = -5   /* no CUDA device, or not an sm_100 part */
+    PD_ENODEV = -5,  /* no CUDA device, or not an sm_100 part */
+    PD_EFORMAT = -6  /* malformed data, e.g. a non-finite matrix element (FormatError) */
 } pd_status;
 
 typedef enum pd_path {
@@ -95,6 +96,17 @@ PD_EXPORT int pd_oracle_coeff(pd_ctx* ctx, unsigned num_qubits, const double* g,
  * (2*4^N doubles). Replaces recompose(const PauliDecomposition&) (decompose.hpp:59,
  * decompose.cpp:221-250). N <= 16. */
 PD_EXPORT int pd_recompose(pd_ctx* ctx, unsigned num_qubits, const double* coeffs, double* g_out);
+
+/* Decompose g and keep on the device only the coefficients with |c_n| > threshold (all when
+ * threshold == 0), in ascending tensor-number order: the selection of the reference's CSV
+ * writer (io.cpp:286-307) done before any D2H. *n_kept receives the count; pd_sparse_fetch
+ * copies the kept tensor numbers and coefficients out. The device selection is a superset
+ * within 1e-12 relative of the threshold; apply |c| > threshold exactly on the host.
+ * check_finite != 0 rejects non-finite elements with PD_EFORMAT (the readers' rule,
+ * io.cpp:118-123), checked on the device copy of g. */
+PD_EXPORT int pd_decompose_sparse(pd_ctx* ctx, unsigned num_qubits, const double* g, pd_path path,
+                                  double threshold, int check_finite, uint64_t* n_kept);
+PD_EXPORT int pd_sparse_fetch(pd_ctx* ctx, uint64_t* idx, double* vals);
 
 /* ---------------- device-resident entry points (stream-ordered) ---------------- */
 
@@ -144,6 +156,15 @@ PD_EXPORT int pd_coeff_batch_device(unsigned num_qubits, const double* g, const 
 /* Device restatement of the reference's seeded generator random_matrix(N, seed)
  * (bench.cpp:16-58); bit-identical to it. */
 PD_EXPORT int pd_random_matrix_device(unsigned num_qubits, uint64_t seed, double* g, void* stream);
+
+/* Index of the first complex element of g[0..count) with a non-finite part, or UINT64_MAX;
+ * synchronous on `stream`. */
+PD_EXPORT int pd_first_nonfinite_device(const double* g, uint64_t count, uint64_t* first,
+                                        void* stream);
+
+/* Page-locked host memory for the host-buffer entry points (H2D/D2H at full PCIe rate). */
+PD_EXPORT int pd_host_alloc(size_t bytes, void** out);
+PD_EXPORT int pd_host_free(void* p);
 
 /* ---------------- measurement helpers ---------------- */
 

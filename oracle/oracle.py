@@ -161,6 +161,16 @@ class Reference:
             getattr(lib, name).argtypes = [ctypes.c_void_p, _u64, _dp]
         lib.pdref_coeff_batch.argtypes = [ctypes.c_void_p, _u64p, _u64, _dp, _uint]
         lib.pdref_recompose.argtypes = [_uint, _dp, _dp]
+        lib.pdref_format_double.argtypes = [ctypes.c_double, ctypes.c_char_p, _uint]
+        lib.pdref_write_matrix_file.argtypes = [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_int]
+        lib.pdref_read_matrix_file.restype = ctypes.c_void_p
+        lib.pdref_read_matrix_file.argtypes = [ctypes.c_char_p, ctypes.c_int]
+        lib.pdref_matrix_qubits.restype = _uint
+        lib.pdref_matrix_qubits.argtypes = [ctypes.c_void_p]
+        lib.pdref_write_coefficients_file.restype = ctypes.c_longlong
+        lib.pdref_write_coefficients_file.argtypes = [_uint, _dp, ctypes.c_char_p, ctypes.c_double]
+        lib.pdref_read_coefficients_file.argtypes = [ctypes.c_char_p, ctypes.POINTER(_uint), _dp,
+                                                     ctypes.c_ulonglong]
         self.lib = lib
         self.cores = int(lib.pdref_hardware_concurrency())
 
@@ -247,6 +257,38 @@ class Reference:
         out = np.empty((2**nq, 2**nq), dtype=np.complex128)
         self._check(self.lib.pdref_recompose(nq, _ptr(c.view(np.float64)), _ptr(out.view(np.float64))))
         return out
+
+    # ---- the reference's file formats (io.cpp) ----
+    def format_double(self, v: float) -> str:
+        buf = ctypes.create_string_buffer(64)
+        assert self.lib.pdref_format_double(v, buf, 64) == 0
+        return buf.value.decode()
+
+    def write_matrix(self, g, path: str, binary: bool) -> None:
+        m = self._h(g)
+        self._check(self.lib.pdref_write_matrix_file(m.h, path.encode(), int(binary)))
+
+    def read_matrix(self, path: str, binary: bool) -> np.ndarray:
+        h = self.lib.pdref_read_matrix_file(path.encode(), int(binary))
+        if not h:
+            raise ValueError(self.lib.pdref_last_error().decode())
+        return Reference.Matrix(self, h, int(self.lib.pdref_matrix_qubits(h))).to_numpy()
+
+    def write_coefficients(self, coeffs, path: str, threshold: float = 0.0) -> int:
+        c = np.ascontiguousarray(coeffs, dtype=np.complex128)
+        nq = (int(c.size).bit_length() - 1) // 2
+        r = self.lib.pdref_write_coefficients_file(nq, _ptr(c.view(np.float64)), path.encode(), threshold)
+        if r < 0:
+            self._check(int(r))
+        return int(r)
+
+    def read_coefficients(self, path: str, max_qubits: int = 10) -> np.ndarray:
+        nq = _uint(0)
+        cap = 4**max_qubits
+        out = np.zeros(cap, dtype=np.complex128)
+        self._check(self.lib.pdref_read_coefficients_file(path.encode(), ctypes.byref(nq),
+                                                          _ptr(out.view(np.float64)), cap))
+        return out[: 4**nq.value].copy()
 
 
 _port = None

@@ -21,6 +21,7 @@
 
 #include "paulidecomp/bench.hpp"
 #include "paulidecomp/decompose.hpp"
+#include "paulidecomp/io.hpp"
 #include "paulidecomp/matrix.hpp"
 
 using namespace paulidecomp;
@@ -159,6 +160,53 @@ int pdref_recompose(unsigned n_qubits, const double* coeffs, double* out) {
         std::memcpy(c.data(), coeffs, total * sizeof(Complex));
         const DenseMatrix m = recompose(PauliDecomposition{n_qubits, std::move(c)});
         copy_out(m.elements(), out);
+    });
+}
+
+// ---- file formats (io.hpp): the reference's own readers/writers ----
+
+int pdref_format_double(double v, char* buf, unsigned cap) {
+    const std::string s = format_double(v);
+    if (s.size() + 1 > cap) return -1;
+    std::memcpy(buf, s.c_str(), s.size() + 1);
+    return 0;
+}
+
+int pdref_write_matrix_file(void* h, const char* path, int binary) {
+    return guarded([&] {
+        write_matrix(*static_cast<DenseMatrix*>(h), path, binary ? MatrixFormat::binary : MatrixFormat::text);
+    });
+}
+
+void* pdref_read_matrix_file(const char* path, int binary) {
+    DenseMatrix* m = nullptr;
+    int rc = guarded([&] {
+        m = new DenseMatrix(read_matrix(path, binary ? MatrixFormat::binary : MatrixFormat::text));
+    });
+    return rc == 0 ? m : nullptr;
+}
+
+unsigned pdref_matrix_qubits(void* h) { return static_cast<DenseMatrix*>(h)->num_qubits(); }
+
+long long pdref_write_coefficients_file(unsigned n_qubits, const double* coeffs, const char* path,
+                                        double threshold) {
+    long long written = -1;
+    int rc = guarded([&] {
+        std::vector<Complex> c(pow4(n_qubits));
+        std::memcpy(c.data(), coeffs, c.size() * sizeof(Complex));
+        written = static_cast<long long>(
+            write_coefficients(PauliDecomposition{n_qubits, std::move(c)}, path, threshold));
+    });
+    return rc == 0 ? written : rc;
+}
+
+// reads a coefficient CSV; *n_qubits receives N, out (capacity cap entries) the 4^N values
+int pdref_read_coefficients_file(const char* path, unsigned* n_qubits, double* out, unsigned long long cap) {
+    return guarded([&] {
+        const PauliDecomposition d = read_coefficients(path);
+        *n_qubits = d.num_qubits;
+        if (d.coefficients.size() <= cap)
+            std::memcpy(out, d.coefficients.data(), d.coefficients.size() * sizeof(Complex));
     });
 }
 

@@ -11,7 +11,10 @@ kernels through the C ABI in ``include/pd_api.h``:
     gray_code, flipped_bit_index, xy_mask, label_to_index, index_to_label, FormatError
 
 B200 additions: ``coefficients`` (batched strings), ``device`` (stream-ordered entry points
-on device pointers), ``sharding`` (X-mask sharding over GPUs with NCCL), ``launch_count``.
+on device pointers), ``sharding`` (X-mask sharding over GPUs with NCCL), ``launch_count``, and
+the reference's file formats (``read_matrix``/``write_matrix``/``read_coefficients``/
+``write_coefficients``/``format_double``) with ``decompose_file`` feeding the GPU directly;
+the ``pdb200`` executable mirrors the reference CLI's decompose/recompose/coeff.
 
 There is no CPU fallback: importing this package without its compiled extension raises,
 and every compute call without an sm_100 GPU raises RuntimeError.
@@ -37,7 +40,9 @@ from ._paulidecomp import (  # noqa: E402
     coefficient,
     coefficients,
     decompose,
+    decompose_file,
     device,
+    format_double,
     flipped_bit_index,
     fp64_add_probe,
     gray_code,
@@ -45,8 +50,12 @@ from ._paulidecomp import (  # noqa: E402
     label_to_index,
     launch_count,
     oracle_coefficient,
+    read_coefficients,
+    read_matrix,
     recompose,
     set_device,
+    write_coefficients,
+    write_matrix,
     xy_mask,
 )
 
@@ -58,7 +67,9 @@ __all__ = [
     "coefficient",
     "coefficients",
     "decompose",
+    "decompose_file",
     "device",
+    "format_double",
     "flipped_bit_index",
     "fp64_add_probe",
     "gray_code",
@@ -66,8 +77,12 @@ __all__ = [
     "label_to_index",
     "launch_count",
     "oracle_coefficient",
+    "read_coefficients",
+    "read_matrix",
     "recompose",
     "set_device",
+    "write_coefficients",
+    "write_matrix",
     "xy_mask",
     "LIBRARY_PATH",
 ]

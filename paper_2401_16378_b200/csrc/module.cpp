@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "paulidecomp_b200/decompose.hpp"
+#include "paulidecomp_b200/io.hpp"
 #include "pd_api.h"
 
 namespace py = pybind11;
@@ -177,6 +178,49 @@ PYBIND11_MODULE(_paulidecomp, m) {
         return r;
     }, py::arg("device") = 0, "Achieved DADD/s of a pure FP64-add kernel on all SMs.");
     m.attr("__version__") = "0.1.0+b200";
+
+    // file formats (proj/docs/formats.md), io.hpp
+    auto mfmt = [](const std::string& f) {
+        if (f == "text") return MatrixFormat::text;
+        if (f == "binary") return MatrixFormat::binary;
+        throw std::invalid_argument("format must be 'text' or 'binary'");
+    };
+    m.def("format_double", &format_double, py::arg("value"),
+          "Shortest round-trip decimal text, '.0' appended to integral values.");
+    m.def("read_matrix", [mfmt](const std::string& path, const std::string& format) {
+        DenseMatrix g = read_matrix(path, mfmt(format));
+        const auto d = static_cast<py::ssize_t>(g.dim());
+        return py::array_t<Complex>({d, d}, g.data());
+    }, py::arg("path"), py::arg("format") = "text");
+    m.def("write_matrix", [mfmt](const ComplexArray& a, const std::string& path, const std::string& format) {
+        const unsigned N = matrix_qubits(a);
+        DenseMatrix g(N, std::vector<Complex>(a.data(), a.data() + a.size()));
+        write_matrix(g, path, mfmt(format));
+    }, py::arg("matrix"), py::arg("path"), py::arg("format") = "text");
+    m.def("read_coefficients", [](const std::string& path) {
+        PauliDecomposition d = read_coefficients(path);
+        return py::array_t<Complex>(static_cast<py::ssize_t>(d.coefficients.size()), d.coefficients.data());
+    }, py::arg("path"));
+    m.def("write_coefficients", [](const ComplexArray& c, const std::string& path, double threshold) {
+        if (c.ndim() != 1) throw std::invalid_argument("coefficients must be a 1-d array");
+        const auto count = static_cast<std::uint64_t>(c.shape(0));
+        if (count < 4 || !std::has_single_bit(count) || (std::countr_zero(count) & 1))
+            throw std::invalid_argument("coefficient count must be a power of four >= 4");
+        PauliDecomposition d{static_cast<unsigned>(std::countr_zero(count) / 2),
+                             std::vector<Complex>(c.data(), c.data() + count)};
+        py::gil_scoped_release nogil;
+        return write_coefficients(d, path, threshold);
+    }, py::arg("coefficients"), py::arg("path"), py::arg("threshold") = 0.0,
+          "Write the coefficient CSV; returns the number of records.");
+    m.def("decompose_file", [mfmt](const std::string& in, const std::string& out, const std::string& format,
+                                   double threshold, const std::string& path) {
+        const MatrixFormat f = mfmt(format);
+        const Path p = parse_path(path);
+        py::gil_scoped_release nogil;
+        return decompose_file(in, f, out, threshold, p);
+    }, py::arg("in_path"), py::arg("out_path"), py::arg("format") = "binary", py::arg("threshold") = 0.0,
+          py::arg("path") = "gray",
+          "Matrix file -> GPU decomposition -> threshold selection on the GPU -> coefficient CSV.");
 
     py::module_ d = m.def_submodule("device", "Stream-ordered entry points on device pointers");
     d.def("scratch_bytes", [](unsigned N, std::uint64_t x_count, const std::string& path) {

@@ -106,6 +106,13 @@ struct pd_ctx {
     cudaEvent_t seg_done = nullptr;
     void* part = nullptr;            // raw partial sums between walk segments
     size_t part_bytes = 0;
+    void* sel_tiles = nullptr;       // threshold selection (pd_decompose_sparse)
+    size_t sel_tiles_bytes = 0;
+    void* sel_idx = nullptr;
+    size_t sel_idx_bytes = 0;
+    void* sel_val = nullptr;
+    size_t sel_val_bytes = 0;
+    uint64_t sel_count = 0;
     void* g = nullptr;
     size_t g_bytes = 0;
     void* out = nullptr;
@@ -186,7 +193,8 @@ int pd_ctx_destroy(pd_ctx* ctx) {
     cudaSetDevice(ctx->device);
     for (cudaStream_t s : {ctx->stream, ctx->stream2, ctx->d2h, ctx->h2d})
         if (s) cudaStreamSynchronize(s);
-    for (void* p : {ctx->g, ctx->out, ctx->scratch, ctx->ns, ctx->part})
+    for (void* p : {ctx->g, ctx->out, ctx->scratch, ctx->ns, ctx->part, ctx->sel_tiles, ctx->sel_idx,
+                    ctx->sel_val})
         if (p) cudaFree(p);
     for (cudaEvent_t ev : {ctx->gathered, ctx->seg_done})
         if (ev) cudaEventDestroy(ev);
@@ -348,10 +356,94 @@ int pd_random_matrix_device(unsigned N, uint64_t seed, double* g, void* stream) 
 
 // ---------------- host-buffer entry points ----------------
 
+namespace {
+int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_path path);
+}
+
 int pd_decompose(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_path path) {
     if (int rc = check_qubits(N)) return rc;
     if (int rc = bind(ctx)) return rc;
     if (!g || !out) return fail(PD_EINVAL, "null buffer");
+    return decompose_host(ctx, N, g, out, path);
+}
+
+int pd_decompose_sparse(pd_ctx* ctx, unsigned N, const double* g, pd_path path, double threshold,
+                        int check_finite, uint64_t* n_kept) {
+    if (int rc = check_qubits(N)) return rc;
+    if (int rc = bind(ctx)) return rc;
+    if (!g || !n_kept) return fail(PD_EINVAL, "null buffer");
+    if (!(threshold >= 0.0)) return fail(PD_EINVAL, "threshold must be non-negative");
+    *n_kept = 0;
+    if (int rc = decompose_host(ctx, N, g, nullptr, path)) return rc;  // coefficients stay on device
+    const uint64_t count = elems(N);
+    if (check_finite) {
+        uint64_t first = 0;
+        if (int rc = pd_first_nonfinite_device(static_cast<const double*>(ctx->g), count, &first,
+                                               ctx->stream))
+            return rc;
+        if (first != UINT64_MAX)
+            return fail(PD_EFORMAT, "non-finite value at row %llu, column %llu",
+                        static_cast<unsigned long long>(first >> N),
+                        static_cast<unsigned long long>(first & ((1ull << N) - 1)));
+    }
+    const uint64_t tiles = pdb::select_tiles(count);
+    if (int rc = ctx->ensure(&ctx->sel_tiles, &ctx->sel_tiles_bytes,
+                             tiles * sizeof(unsigned) + (tiles + 1) * sizeof(unsigned long long) + 64))
+        return rc;
+    if (int rc = ctx->ensure(&ctx->sel_idx, &ctx->sel_idx_bytes, count * sizeof(uint64_t))) return rc;
+    if (int rc = ctx->ensure(&ctx->sel_val, &ctx->sel_val_bytes, count * sizeof(double2))) return rc;
+    unsigned* tile_counts = static_cast<unsigned*>(ctx->sel_tiles);
+    unsigned long long* tile_offsets = reinterpret_cast<unsigned long long*>(
+        static_cast<char*>(ctx->sel_tiles) + ((tiles * sizeof(unsigned) + 63) & ~size_t{63}));
+    // a slightly lowered device threshold keeps a superset; the host applies the exact
+    // std::abs(c) > threshold test of io.cpp:300 to the candidates
+    const double t_dev = threshold > 0.0 ? threshold * (1.0 - 1e-12) : 0.0;
+    cudaError_t e = pdb::launch_select(static_cast<const double2*>(ctx->out), count, t_dev,
+                                       tile_counts, tile_offsets, static_cast<uint64_t*>(ctx->sel_idx),
+                                       static_cast<double2*>(ctx->sel_val), ctx->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "select launch");
+    unsigned long long kept = 0;
+    PD_CUDA(cudaMemcpyAsync(&kept, tile_offsets + tiles, sizeof(kept), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    PD_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->sel_count = kept;
+    *n_kept = kept;
+    return PD_OK;
+}
+
+int pd_sparse_fetch(pd_ctx* ctx, uint64_t* idx, double* vals) {
+    if (int rc = bind(ctx)) return rc;
+    if (ctx->sel_count == 0) return PD_OK;
+    if (!idx || !vals) return fail(PD_EINVAL, "null buffer");
+    PD_CUDA(cudaMemcpyAsync(idx, ctx->sel_idx, ctx->sel_count * sizeof(uint64_t),
+                            cudaMemcpyDeviceToHost, ctx->stream));
+    PD_CUDA(cudaMemcpyAsync(vals, ctx->sel_val, ctx->sel_count * sizeof(double2),
+                            cudaMemcpyDeviceToHost, ctx->stream));
+    PD_CUDA(cudaStreamSynchronize(ctx->stream));
+    return PD_OK;
+}
+
+int pd_first_nonfinite_device(const double* g, uint64_t count, uint64_t* first, void* stream) {
+    if (int rc = check_device()) return rc;
+    if (!first) return fail(PD_EINVAL, "null output");
+    unsigned long long* d = nullptr;
+    PD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(*d), static_cast<cudaStream_t>(stream)));
+    cudaError_t e = pdb::launch_first_nonfinite(reinterpret_cast<const double2*>(g), count, d,
+                                                static_cast<cudaStream_t>(stream));
+    unsigned long long h = ~0ull;
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, static_cast<cudaStream_t>(stream));
+    cudaFreeAsync(d, static_cast<cudaStream_t>(stream));
+    if (e == cudaSuccess) e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "first_nonfinite");
+    *first = h;
+    return PD_OK;
+}
+
+namespace {
+
+// the host-buffer decomposition; out == nullptr leaves the coefficients in ctx->out
+int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_path path) {
     const size_t bytes = elems(N) * sizeof(double2);
     if (int rc = ctx->ensure(&ctx->g, &ctx->g_bytes, bytes)) return rc;
     if (int rc = ctx->ensure(&ctx->out, &ctx->out_bytes, bytes)) return rc;
@@ -364,7 +456,7 @@ int pd_decompose(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_path 
                                          static_cast<double*>(ctx->out), ctx->scratch, path,
                                          ctx->stream))
             return rc;
-        PD_CUDA(cudaMemcpyAsync(out, ctx->out, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+        if (out) PD_CUDA(cudaMemcpyAsync(out, ctx->out, bytes, cudaMemcpyDeviceToHost, ctx->stream));
         PD_CUDA(cudaStreamSynchronize(ctx->stream));
         return PD_OK;
     }
@@ -438,7 +530,7 @@ int pd_decompose(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_path 
         if (rc) return rc;
         PD_CUDA(cudaEventRecord(ctx->block_done[q], s));
         PD_CUDA(cudaStreamWaitEvent(ctx->d2h, ctx->block_done[q], 0));
-        for (unsigned r = 0; r < (1u << kBits); ++r) {
+        for (unsigned r = 0; out && r < (1u << kBits); ++r) {
             const uint64_t off = 2 * pd_run_offset(N, kBits, q, r);
             PD_CUDA(cudaMemcpyAsync(out + off, dout + off, run * sizeof(double2),
                                     cudaMemcpyDeviceToHost, ctx->d2h));
@@ -450,6 +542,8 @@ int pd_decompose(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_path 
     PD_CUDA(cudaStreamSynchronize(ctx->h2d));
     return PD_OK;
 }
+
+}  // namespace
 
 int pd_recompose(pd_ctx* ctx, unsigned N, const double* coeffs, double* g_out) {
     if (int rc = check_qubits(N)) return rc;
@@ -527,6 +621,19 @@ int pd_oracle_coeff(pd_ctx* ctx, unsigned N, const double* g, uint64_t n, double
     if (e != cudaSuccess) return cuda_fail(e, "kron_trace launch");
     PD_CUDA(cudaMemcpyAsync(out, ctx->out, sizeof(double2), cudaMemcpyDeviceToHost, ctx->stream));
     PD_CUDA(cudaStreamSynchronize(ctx->stream));
+    return PD_OK;
+}
+
+int pd_host_alloc(size_t bytes, void** out) {
+    if (!out) return fail(PD_EINVAL, "null output pointer");
+    *out = nullptr;
+    if (int rc = check_device()) return rc;
+    PD_CUDA(cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocDefault));
+    return PD_OK;
+}
+
+int pd_host_free(void* p) {
+    if (p) PD_CUDA(cudaFreeHost(p));
     return PD_OK;
 }
 

@@ -64,6 +64,14 @@ cudaError_t launch_walk(const double2* G, unsigned N, const uint64_t* ns, uint64
 cudaError_t launch_kron_trace(const double2* G, unsigned N, uint64_t n, double2* out,
                               cudaStream_t stream);
 
+// file-path helpers (pd_io.cu)
+cudaError_t launch_first_nonfinite(const double2* v, uint64_t count, unsigned long long* result,
+                                   cudaStream_t stream);
+uint64_t select_tiles(uint64_t count);
+cudaError_t launch_select(const double2* c, uint64_t count, double threshold, unsigned* tile_counts,
+                          unsigned long long* tile_offsets, uint64_t* idx_out, double2* val_out,
+                          cudaStream_t stream);
+
 cudaError_t launch_random_matrix(unsigned N, uint64_t seed, double2* out, cudaStream_t stream);
 
 cudaError_t launch_fp64_probe(unsigned blocks, unsigned iters, double* sink, cudaStream_t stream);
