@@ -382,6 +382,8 @@ def run_ours(args) -> None:
                                              "kernel": "K4 fused two-pass WHT", "k4_ms": k4w}}
             line["wht_path"]["roofline"]["frac"] = (line["wht_path"]["roofline"]["achieved"]
                                                     / line["wht_path"]["roofline"]["peak"])
+        if world == 1 and rank == 0:
+            line["side_configs"] = side_configs(pd, dev, stream, sptr, peaks)
 
     # ---- e2e through the public API with pinned host buffers (H2D + D2H inside)
     if not args.no_e2e:
@@ -393,6 +395,50 @@ def run_ours(args) -> None:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def side_configs(pd, dev, stream, sptr, peaks):
+    """The other BASELINE configs on one GPU, device-resident, CUDA events, 3 warm-ups:
+    configs[3] (full N=12 decomposition, the metric's other size) and configs[1] (65,536
+    batched single strings at N=10)."""
+    import numpy as np
+    import torch
+
+    def ev_time(fn, reps):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps
+
+    res = {}
+    nq = 12
+    g = torch.empty((2**nq, 2**nq), dtype=torch.complex128, device=dev)
+    gen = np.random.default_rng(12)
+    g.copy_(torch.from_numpy(gen.standard_normal((2**nq, 2**nq)) + 1j * gen.standard_normal((2**nq, 2**nq))))
+    out = torch.empty(4**nq, dtype=torch.complex128, device=dev)
+    scr = torch.empty(4**nq, dtype=torch.complex128, device=dev)
+    ms = ev_time(lambda: pd.device.decompose(nq, g.data_ptr(), out.data_ptr(), scr.data_ptr(), "gray", sptr), 10)
+    dadd = 2.0 * 2**nq * 4**nq
+    peak = SM_COUNT * FP64_LANES_PER_SM * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+    res["n12_full_gray"] = {"config": "BASELINE configs[3]: full N=12, N(0,1) complex128",
+                            "value": 4**nq / (ms / 1e3), "unit": UNIT, "ms_per_step": ms,
+                            "fp64_frac_incl_k1": dadd / (ms / 1e3) / peak}
+    nq = 10
+    g = torch.empty((2**nq, 2**nq), dtype=torch.complex128, device=dev)
+    g.copy_(torch.from_numpy(gen.standard_normal((2**nq, 2**nq)) + 1j * gen.standard_normal((2**nq, 2**nq))))
+    ns = torch.from_numpy(gen.integers(0, 4**nq, 65536).astype(np.int64)).to(dev)
+    o = torch.empty(65536, dtype=torch.complex128, device=dev)
+    ms = ev_time(lambda: pd.device.coeff_batch(nq, g.data_ptr(), ns.data_ptr(), 65536, False, o.data_ptr(), sptr), 20)
+    res["n10_strings"] = {"config": "BASELINE configs[1]: 65,536 random strings of an N=10 matrix",
+                          "value": 65536 / (ms / 1e3), "unit": "strings/s", "ms_per_step": ms,
+                          "l2_gbs": 65536 * 16.0 * 2**nq / (ms / 1e3) / 1e9}
+    return res
 
 
 def run_e2e(args, pd, plan, G, out, dev, stream, barrier, max_over_ranks, world, rank):

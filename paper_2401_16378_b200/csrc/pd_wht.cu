@@ -265,6 +265,78 @@ __global__ void __launch_bounds__(kWhtThreads, 2)
     }
 }
 
+// Pass 2 for HB = N - 7 in [4, 8]: every thread holds 16 elements in both register rounds.
+// Round A loads straight from D' (128 B pieces, 4 per warp load) and butterflies high bits
+// [0, 4); one shared-memory exchange; round B butterflies bits [4, HB) and writes the
+// coefficients from registers (a warp covers 32 consecutive (x_low, j) columns: two 256 B runs).
+// 2 shared-memory accesses and 1 barrier per element (the generic kernel above needs 6 and 3).
+template <int HB>
+__global__ void __launch_bounds__(kWhtThreads, 2)
+    wht_hi_reg_kernel(const double2* __restrict__ dprime, unsigned N, uint64_t x0,
+                      unsigned run_bits, Runs runs, double scale) {
+    static_assert(HB >= 4 && HB <= 8, "16 elements per thread in both rounds");
+    extern __shared__ __align__(16) double2 s2[];             // [2^HB][COLS]
+    constexpr int RB = HB - 4;                                 // bits of round B
+    constexpr unsigned COLS = 1u << (12 - HB);                 // (x_low, j) columns per CTA
+    constexpr unsigned XPC_LOG = 9 - HB;                       // X-masks per CTA = COLS / 8
+    constexpr int PAIRS = 1 << (8 - HB);                       // (hi_low, col) pairs per thread
+    const uint64_t dim = 1ull << N;
+    const uint64_t jb = blockIdx.x & 15;
+    const uint64_t xq = blockIdx.x >> 4;
+    {
+        const unsigned col = threadIdx.x % COLS, a = threadIdx.x / COLS;
+        const double2* src = dprime + ((xq << XPC_LOG) + (col >> 3)) * dim + (jb << 3) + (col & 7);
+        double2 v[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r)
+            v[r] = __ldcs(src + (static_cast<uint64_t>((a << 4) | r) << kLoBits));
+#pragma unroll
+        for (int h = 1; h < 16; h <<= 1)
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                if (k & h) continue;
+                const double2 p = v[k], q = v[k + h];
+                v[k] = make_double2(p.x + q.x, p.y + q.y);
+                v[k + h] = make_double2(p.x - q.x, p.y - q.y);
+            }
+#pragma unroll
+        for (int r = 0; r < 16; ++r) s2[((a << 4) | r) * COLS + col] = v[r];
+    }
+    __syncthreads();
+    const unsigned low_bits = 2 * (N - run_bits);
+    const uint64_t low_mask = (low_bits >= 64) ? ~0ull : ((1ull << low_bits) - 1);
+#pragma unroll
+    for (int q = 0; q < PAIRS; ++q) {
+        const unsigned p = threadIdx.x + q * kWhtThreads;
+        const unsigned col = p % COLS, hlo = p / COLS;
+        double2 v[1 << RB];
+#pragma unroll
+        for (int h = 0; h < (1 << RB); ++h) v[h] = s2[((h << 4) | hlo) * COLS + col];
+#pragma unroll
+        for (int h = 1; h < (1 << RB); h <<= 1)
+#pragma unroll
+            for (int k = 0; k < (1 << RB); ++k) {
+                if (k & h) continue;
+                const double2 a = v[k], b = v[k + h];
+                v[k] = make_double2(a.x + b.x, a.y + b.y);
+                v[k + h] = make_double2(a.x - b.x, a.y - b.y);
+            }
+        const uint64_t x = x0 + (xq << XPC_LOG) + (col >> 3);
+#pragma unroll
+        for (int h = 0; h < (1 << RB); ++h) {
+            const uint64_t z = (static_cast<uint64_t>((h << 4) | hlo) << kLoBits) | (jb << 3) | (col & 7);
+            const unsigned ph = (3u * static_cast<unsigned>(__popcll(x & z))) & 3u;
+            const uint64_t n = tensor_number(x, z);
+            const unsigned run = static_cast<unsigned>(z >> (N - run_bits));
+            double2* dst = runs.ptr[0];
+#pragma unroll
+            for (unsigned r = 1; r < kMaxRuns; ++r)
+                if (run == r) dst = runs.ptr[r];
+            __stcs(&dst[n & low_mask], apply_phase(ph, v[h].x, v[h].y, scale));
+        }
+    }
+}
+
 }  // namespace
 
 // shared driver: rows pass, then (N > 12) the column pass; emit != 0 writes
@@ -309,6 +381,34 @@ cudaError_t launch_wht_xmask(const double2* diag_c, unsigned N, uint64_t x0, uin
     return wht_passes(const_cast<double2*>(diag_c), N, x0, x_count, run_bits, runs, 1, stream);
 }
 
+// pass 2 dispatch: the register-round kernel for HB in [4, 8], the generic one otherwise
+static cudaError_t launch_pass2(const double2* scratch, unsigned N, uint64_t x0, uint64_t x_count,
+                                unsigned run_bits, const Runs& runs, cudaStream_t stream) {
+    const unsigned hb = N - kLoBits;
+    if (hb < 4 || hb > 8 || x_count < (1ull << (9 - hb))) return cudaErrorNotSupported;
+    const double scale = 1.0 / static_cast<double>(1ull << N);
+    const size_t smem = sizeof(double2) * 4096;
+    const unsigned grid = static_cast<unsigned>((x_count >> (9 - hb)) << 4);
+    cudaError_t e = cudaSuccess;
+#define PD_REG(HBV)                                                                              \
+    do {                                                                                         \
+        auto k = wht_hi_reg_kernel<HBV>;                                                         \
+        e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);         \
+        if (e == cudaSuccess) k<<<grid, kWhtThreads, smem, stream>>>(scratch, N, x0, run_bits, runs, scale); \
+    } while (0)
+    switch (hb) {
+        case 4: PD_REG(4); break;
+        case 5: PD_REG(5); break;
+        case 6: PD_REG(6); break;
+        case 7: PD_REG(7); break;
+        default: PD_REG(8); break;
+    }
+#undef PD_REG
+    if (e != cudaSuccess) return e;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cudaGetLastError();
+}
+
 bool wht_fused_ok(unsigned N, uint64_t x_count) { return N >= 8 && N <= 16 && x_count >= 32; }
 
 cudaError_t launch_wht_from_matrix(const double2* G, unsigned N, uint64_t x0, uint64_t x_count,
@@ -330,6 +430,11 @@ cudaError_t launch_wht_from_matrix(const double2* G, unsigned N, uint64_t x0, ui
     g_launches.fetch_add(1, std::memory_order_relaxed);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
+    if (launch_pass2(scratch, N, x0, x_count, run_bits, runs, stream) == cudaSuccess) {
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        return cudaGetLastError();
+    }
+    cudaGetLastError();  // clear cudaErrorNotSupported: fall back to the generic pass 2
     const unsigned hb = N - kLoBits;
     const double scale = 1.0 / static_cast<double>(1ull << N);
     // X-masks per CTA: 4 while 2^(hb+3) <= 1024, then 2, then 1 (<= 4096 elements, 68 KiB)
