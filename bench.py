@@ -238,11 +238,10 @@ def run_ours(args) -> None:
     out = torch.empty(4**nq, dtype=torch.complex128, device=dev) if rank == 0 else None
     local = None if rank == 0 else torch.empty(plan.run_len << plan.run_bits,
                                                dtype=torch.complex128, device=dev)
-    if rank == 0:
-        runs = [out[o:o + plan.run_len] for o in plan.offsets()]
-    else:
-        runs = [local[r * plan.run_len:(r + 1) * plan.run_len] for r in range(1 << plan.run_bits)]
-    run_ptrs = [r.data_ptr() for r in runs]
+    # rank 0 writes its runs in place in the reference-ordered array; the others pack theirs
+    dst, layout = (out, "global") if rank == 0 else (local, "runs")
+    runs = [] if rank == 0 else \
+        [local[r * plan.run_len:(r + 1) * plan.run_len] for r in range(1 << plan.run_bits)]
 
     def gather():
         if world == 1:
@@ -268,12 +267,12 @@ def run_ours(args) -> None:
             if ev is not None:
                 ev[1].record(stream)
             pd.device.xmask_coeffs(nq, diag.data_ptr(), plan.x0, plan.x_count, plan.run_bits,
-                                   run_ptrs, path, sptr)
+                                   dst.data_ptr(), layout, path, sptr)
         else:  # fused two-pass WHT straight from G
             if ev is not None:
                 ev[1].record(stream)
             pd.device.shard_coeffs(nq, G.data_ptr(), plan.x0, plan.x_count, plan.run_bits,
-                                   run_ptrs, diag.data_ptr(), path, sptr)
+                                   dst.data_ptr(), layout, diag.data_ptr(), path, sptr)
         if ev is not None:
             ev[2].record(stream)
         gather()

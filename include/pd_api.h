@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define PD_API_VERSION 1
+#define PD_API_VERSION 2
 
 #if defined(__GNUC__)
 #define PD_EXPORT __attribute__((visibility("default")))
@@ -57,6 +57,13 @@ typedef enum pd_path {
     PD_PATH_WHT = 1,   /* K1 + fast Walsh-Hadamard butterflies (separately reported second path) */
     PD_PATH_NAIVE = 2  /* K0: one thread per n, reference-order walk straight from G */
 } pd_path;
+
+/* Where the coefficients of an X-mask range go (pd_xmask_coeffs_device, pd_shard_coeffs_device). */
+typedef enum pd_layout {
+    PD_LAYOUT_GLOBAL = 0, /* out[n]: the reference-ordered array of all 4^N coefficients */
+    PD_LAYOUT_RUNS = 1    /* out is the range's block of 4^N / 2^run_bits coefficients, packed
+                             as its 2^run_bits runs (see pd_xmask_coeffs_device) */
+} pd_layout;
 
 typedef struct pd_ctx pd_ctx;
 
@@ -125,22 +132,25 @@ PD_EXPORT int pd_diag_gather_device(unsigned num_qubits, const double* g, uint64
 
 /* K2 (path GRAY) or K4 (path WHT): every coefficient whose X-mask lies in
  * [x0, x0 + x_count), from the gathered diagonals. Output addressing follows the
- * X-mask sharding of the multi-GPU layer: with run_bits = p, X-mask shard
- * g = x0 >> (N - p) owns 2^p contiguous runs of 4^(N-p) coefficients of the
- * reference-ordered array, one per value of the top p bits of the Z-mask;
- * run_out[r] receives the run for Z-mask top bits r (2^p device pointers).
- * p = 0 with run_out[0] = out writes the plain reference-ordered array. */
+ * X-mask sharding of the multi-GPU layer: with run_bits = p, the X-masks whose top p
+ * bits equal g (block g of 2^p) own 2^p contiguous runs of 4^(N-p) coefficients of the
+ * reference-ordered array, one per value r of the top p bits of the Z-mask, starting at
+ * pd_run_offset(N, p, g, r). The range must lie inside one such block.
+ *   PD_LAYOUT_GLOBAL: coefficient n goes to out[n] (out holds all 4^N; p is irrelevant).
+ *   PD_LAYOUT_RUNS:   out holds the block's runs back to back: run r at out + r 4^(N-p),
+ *                     so a block (a GPU's shard, or one pipelined sub-block) is contiguous.
+ * p <= min(N, 8). out is 2 doubles per coefficient. */
 PD_EXPORT int pd_xmask_coeffs_device(unsigned num_qubits, const double* diag, uint64_t x0, uint64_t x_count,
-                           unsigned run_bits, double* const* run_out, pd_path path, void* stream);
+                           unsigned run_bits, double* out, pd_layout layout, pd_path path, void* stream);
 
 /* Every coefficient whose X-mask lies in [x0, x0 + x_count), straight from the matrix g,
- * with the run addressing of pd_xmask_coeffs_device. GRAY: K1 into scratch, then K2.
+ * with the output addressing of pd_xmask_coeffs_device. GRAY: K1 into scratch, then K2.
  * WHT: the fused two-pass transform (pass 1 gathers and butterflies the low 7 index bits
  * into scratch, pass 2 the high bits) when N in [8,16] and x_count >= 32, else K1 + K4.
  * scratch >= pd_scratch_bytes(N, x_count, path). This is one X-mask shard's work. */
 PD_EXPORT int pd_shard_coeffs_device(unsigned num_qubits, const double* g, uint64_t x0,
-                                     uint64_t x_count, unsigned run_bits, double* const* run_out,
-                                     void* scratch, pd_path path, void* stream);
+                                     uint64_t x_count, unsigned run_bits, double* out,
+                                     pd_layout layout, void* scratch, pd_path path, void* stream);
 
 /* Global offset (in coefficients) of run r of X-mask shard g for p = run_bits. */
 PD_EXPORT uint64_t pd_run_offset(unsigned num_qubits, unsigned run_bits, uint64_t shard, uint64_t run);

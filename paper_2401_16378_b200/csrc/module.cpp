@@ -240,28 +240,30 @@ PYBIND11_MODULE(_paulidecomp, m) {
                                     P<void>(stream)));
     }, py::arg("num_qubits"), py::arg("g"), py::arg("x0"), py::arg("x_count"), py::arg("diag"),
           py::arg("stream") = 0);
-    d.def("xmask_coeffs", [](unsigned N, std::uintptr_t diag, std::uint64_t x0, std::uint64_t x_count,
-                             unsigned run_bits, const std::vector<std::uintptr_t>& runs,
-                             const std::string& path, std::uintptr_t stream) {
-        if (runs.size() != (std::size_t{1} << run_bits))
-            throw std::invalid_argument("need 2**run_bits run pointers");
-        std::vector<double*> rp(runs.size());
-        for (std::size_t r = 0; r < runs.size(); ++r) rp[r] = P<double>(runs[r]);
-        check(pd_xmask_coeffs_device(N, P<const double>(diag), x0, x_count, run_bits, rp.data(),
-                                     path_of(path), P<void>(stream)));
+    auto layout_of = [](const std::string& l) {
+        if (l == "global") return PD_LAYOUT_GLOBAL;
+        if (l == "runs") return PD_LAYOUT_RUNS;
+        throw std::invalid_argument("layout must be 'global' or 'runs'");
+    };
+    d.def("xmask_coeffs", [layout_of](unsigned N, std::uintptr_t diag, std::uint64_t x0,
+                                      std::uint64_t x_count, unsigned run_bits, std::uintptr_t out,
+                                      const std::string& layout, const std::string& path,
+                                      std::uintptr_t stream) {
+        check(pd_xmask_coeffs_device(N, P<const double>(diag), x0, x_count, run_bits, P<double>(out),
+                                     layout_of(layout), path_of(path), P<void>(stream)));
     }, py::arg("num_qubits"), py::arg("diag"), py::arg("x0"), py::arg("x_count"),
-          py::arg("run_bits"), py::arg("runs"), py::arg("path") = "gray", py::arg("stream") = 0);
-    d.def("shard_coeffs", [](unsigned N, std::uintptr_t g, std::uint64_t x0, std::uint64_t x_count,
-                             unsigned run_bits, const std::vector<std::uintptr_t>& runs,
-                             std::uintptr_t scratch, const std::string& path, std::uintptr_t stream) {
-        if (runs.size() != (std::size_t{1} << run_bits))
-            throw std::invalid_argument("need 2**run_bits run pointers");
-        std::vector<double*> rp(runs.size());
-        for (std::size_t r = 0; r < runs.size(); ++r) rp[r] = P<double>(runs[r]);
-        check(pd_shard_coeffs_device(N, P<const double>(g), x0, x_count, run_bits, rp.data(),
-                                     P<void>(scratch), path_of(path), P<void>(stream)));
+          py::arg("run_bits"), py::arg("out"), py::arg("layout") = "global", py::arg("path") = "gray",
+          py::arg("stream") = 0);
+    d.def("shard_coeffs", [layout_of](unsigned N, std::uintptr_t g, std::uint64_t x0,
+                                      std::uint64_t x_count, unsigned run_bits, std::uintptr_t out,
+                                      const std::string& layout, std::uintptr_t scratch,
+                                      const std::string& path, std::uintptr_t stream) {
+        check(pd_shard_coeffs_device(N, P<const double>(g), x0, x_count, run_bits, P<double>(out),
+                                     layout_of(layout), P<void>(scratch), path_of(path),
+                                     P<void>(stream)));
     }, py::arg("num_qubits"), py::arg("g"), py::arg("x0"), py::arg("x_count"), py::arg("run_bits"),
-          py::arg("runs"), py::arg("scratch"), py::arg("path") = "gray", py::arg("stream") = 0,
+          py::arg("out"), py::arg("layout") = "global", py::arg("scratch") = 0,
+          py::arg("path") = "gray", py::arg("stream") = 0,
           "All coefficients of an X-mask range straight from G (one shard's work).");
     d.def("coeff_batch", [](unsigned N, std::uintptr_t g, std::uintptr_t ns, std::uint64_t count,
                             bool slow, std::uintptr_t out, std::uintptr_t stream) {

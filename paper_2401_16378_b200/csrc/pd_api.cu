@@ -239,30 +239,37 @@ int pd_diag_gather_device(unsigned N, const double* g, uint64_t x0, uint64_t x_c
     return PD_OK;
 }
 
-int pd_xmask_coeffs_device(unsigned N, const double* diag, uint64_t x0, uint64_t x_count,
-                           unsigned run_bits, double* const* run_out, pd_path path, void* stream) {
-    if (int rc = check_qubits(N)) return rc;
-    if (int rc = check_device()) return rc;
+namespace {
+int check_xrange(unsigned N, uint64_t x0, uint64_t x_count, unsigned run_bits, const double* out,
+                 pd_layout layout) {
     if (run_bits > pdb::kMaxRunBits || run_bits > N)
-        return fail(PD_EINVAL, "run_bits must be <= min(3, N)");
+        return fail(PD_EINVAL, "run_bits must be <= min(%u, N)", pdb::kMaxRunBits);
     if (x_count == 0 || (x_count & (x_count - 1)) || x0 % x_count || x0 + x_count > (1ull << N))
         return fail(PD_EINVAL, "X-mask range must be an aligned power-of-two block inside [0, 2^N)");
     if (x_count > (1ull << (N - run_bits)))
-        return fail(PD_EINVAL, "X-mask range spans more than one shard");
-    if (!run_out) return fail(PD_EINVAL, "null run_out");
-    double2* runs[pdb::kMaxRuns] = {};
-    for (unsigned r = 0; r < (1u << run_bits); ++r) {
-        if (!run_out[r]) return fail(PD_EINVAL, "null run_out[%u]", r);
-        runs[r] = reinterpret_cast<double2*>(run_out[r]);
-    }
+        return fail(PD_EINVAL, "X-mask range spans more than one block of 2^(N - run_bits)");
+    if (layout != PD_LAYOUT_GLOBAL && layout != PD_LAYOUT_RUNS)
+        return fail(PD_EINVAL, "layout must be PD_LAYOUT_GLOBAL or PD_LAYOUT_RUNS");
+    if (!out) return fail(PD_EINVAL, "null output");
+    return PD_OK;
+}
+}  // namespace
+
+int pd_xmask_coeffs_device(unsigned N, const double* diag, uint64_t x0, uint64_t x_count,
+                           unsigned run_bits, double* out, pd_layout layout, pd_path path,
+                           void* stream) {
+    if (int rc = check_qubits(N)) return rc;
+    if (int rc = check_device()) return rc;
+    if (int rc = check_xrange(N, x0, x_count, run_bits, out, layout)) return rc;
     cudaError_t e;
     const double2* d = reinterpret_cast<const double2*>(diag);
+    double2* o = reinterpret_cast<double2*>(out);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     switch (path) {
-        case PD_PATH_GRAY: e = pdb::launch_gray_xmask(d, N, x0, x_count, run_bits, runs, s); break;
+        case PD_PATH_GRAY: e = pdb::launch_gray_xmask(d, N, x0, x_count, run_bits, o, layout, s); break;
         case PD_PATH_WHT:
             if (N > 16) return fail(PD_EINVAL, "the WHT path supports N <= 16");
-            e = pdb::launch_wht_xmask(d, N, x0, x_count, run_bits, runs, s);
+            e = pdb::launch_wht_xmask(d, N, x0, x_count, run_bits, o, layout, s);
             break;
         default: return fail(PD_EINVAL, "path must be PD_PATH_GRAY or PD_PATH_WHT");
     }
@@ -271,34 +278,27 @@ int pd_xmask_coeffs_device(unsigned N, const double* diag, uint64_t x0, uint64_t
 }
 
 int pd_shard_coeffs_device(unsigned N, const double* g, uint64_t x0, uint64_t x_count,
-                           unsigned run_bits, double* const* run_out, void* scratch, pd_path path,
-                           void* stream) {
+                           unsigned run_bits, double* out, pd_layout layout, void* scratch,
+                           pd_path path, void* stream) {
     if (int rc = check_qubits(N)) return rc;
     if (int rc = check_device()) return rc;
     if (!g || !scratch) return fail(PD_EINVAL, "null buffer");
     if (path == PD_PATH_WHT && pdb::wht_fused_ok(N, x_count)) {
-        if (run_bits > pdb::kMaxRunBits || run_bits > N)
-            return fail(PD_EINVAL, "run_bits must be <= min(3, N)");
-        if (x_count == 0 || (x_count & (x_count - 1)) || x0 % x_count || x0 + x_count > (1ull << N) ||
-            x_count > (1ull << (N - run_bits)))
-            return fail(PD_EINVAL, "X-mask range must be an aligned power-of-two block of one shard");
-        double2* runs[pdb::kMaxRuns] = {};
-        for (unsigned r = 0; r < (1u << run_bits); ++r) {
-            if (!run_out || !run_out[r]) return fail(PD_EINVAL, "null run_out[%u]", r);
-            runs[r] = reinterpret_cast<double2*>(run_out[r]);
-        }
+        if (int rc = check_xrange(N, x0, x_count, run_bits, out, layout)) return rc;
         cudaError_t e = pdb::launch_wht_from_matrix(reinterpret_cast<const double2*>(g), N, x0,
                                                     x_count, static_cast<double2*>(scratch),
-                                                    run_bits, runs, static_cast<cudaStream_t>(stream));
+                                                    run_bits, reinterpret_cast<double2*>(out),
+                                                    layout, static_cast<cudaStream_t>(stream));
         if (e != cudaSuccess) return cuda_fail(e, "fused WHT launch");
         return PD_OK;
     }
     if (path != PD_PATH_GRAY && path != PD_PATH_WHT)
         return fail(PD_EINVAL, "path must be PD_PATH_GRAY or PD_PATH_WHT");
+    if (int rc = check_xrange(N, x0, x_count, run_bits, out, layout)) return rc;
     if (int rc = pd_diag_gather_device(N, g, x0, x_count, static_cast<double*>(scratch), stream))
         return rc;
     return pd_xmask_coeffs_device(N, static_cast<const double*>(scratch), x0, x_count, run_bits,
-                                  run_out, path, stream);
+                                  out, layout, path, stream);
 }
 
 int pd_decompose_device(unsigned N, const double* g, double* out, void* scratch, pd_path path,
@@ -314,8 +314,8 @@ int pd_decompose_device(unsigned N, const double* g, double* out, void* scratch,
     }
     if (path != PD_PATH_GRAY && path != PD_PATH_WHT) return fail(PD_EINVAL, "unknown path");
     if (!scratch) return fail(PD_EINVAL, "null scratch");
-    double* runs[1] = {out};
-    return pd_shard_coeffs_device(N, g, 0, 1ull << N, 0, runs, scratch, path, stream);
+    return pd_shard_coeffs_device(N, g, 0, 1ull << N, 0, out, PD_LAYOUT_GLOBAL, scratch, path,
+                                  stream);
 }
 
 int pd_coeff_batch_device(unsigned N, const double* g, const uint64_t* ns, uint64_t count, int slow,
@@ -501,7 +501,7 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
             cudaError_t e = pdb::launch_gray_segment(reinterpret_cast<const double2*>(diag), N, 0,
                                                      dim, sg * per, (sg + 1) * per,
                                                      sg ? part : nullptr, part, 0, nullptr,
-                                                     ctx->stream);
+                                                     PD_LAYOUT_GLOBAL, ctx->stream);
             if (e != cudaSuccess) return cuda_fail(e, "gray segment launch");
         }
         c_last = (segs - 1) * per;
@@ -513,19 +513,19 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
         PD_CUDA(cudaEventRecord(ctx->gathered, ctx->stream));
     }
     PD_CUDA(cudaStreamWaitEvent(ctx->stream2, ctx->gathered, 0));
-    double* runs[1] = {dout};
     for (unsigned q = 0; q < (1u << kBits); ++q) {
         cudaStream_t s = (q & 1) ? ctx->stream2 : ctx->stream;
         int rc;
         if (gray) {
-            double2* out_runs[1] = {reinterpret_cast<double2*>(dout)};
             cudaError_t e = pdb::launch_gray_segment(
                 reinterpret_cast<const double2*>(diag) + q * xc * dim, N, q * xc, xc, c_last, 0,
-                part ? part + q * xc * dim : nullptr, nullptr, 0, out_runs, s);
+                part ? part + q * xc * dim : nullptr, nullptr, 0,
+                reinterpret_cast<double2*>(dout), PD_LAYOUT_GLOBAL, s);
             rc = e == cudaSuccess ? PD_OK : cuda_fail(e, "gray block launch");
         } else {
             // WHT: each block gathers and transforms its own X-masks from G (fused two-pass)
-            rc = pd_shard_coeffs_device(N, gdev, q * xc, xc, 0, runs, diag + 2 * q * xc * dim, path, s);
+            rc = pd_shard_coeffs_device(N, gdev, q * xc, xc, 0, dout, PD_LAYOUT_GLOBAL,
+                                        diag + 2 * q * xc * dim, path, s);
         }
         if (rc) return rc;
         PD_CUDA(cudaEventRecord(ctx->block_done[q], s));

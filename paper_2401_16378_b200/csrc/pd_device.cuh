@@ -82,6 +82,28 @@ __device__ __forceinline__ double2 apply_phase(unsigned p, double sr, double si,
     return make_double2(cr * scale, ci * scale);
 }
 
+// Where coefficient (x, z) with tensor number n goes (see pd_api.h, pd_layout):
+//   GLOBAL: out[n], the reference-ordered array of all 4^N coefficients;
+//   RUNS:   the coefficients of one aligned block of 2^(N - rb) X-masks, packed as its 2^rb
+//           runs (one per value r of the Z-mask's top rb bits) of 4^(N - rb) entries each:
+//           out[(r << 2(N - rb)) | (n mod 4^(N - rb))].
+struct OutMap {
+    double2* out;
+    unsigned rb_shift;   // N - rb
+    unsigned low_bits;   // 2 (N - rb)
+    int runs;            // 0 GLOBAL, 1 RUNS
+};
+
+__host__ __device__ __forceinline__ uint64_t out_index(const OutMap& m, uint64_t n, uint64_t z) {
+    if (!m.runs) return n;
+    const uint64_t low = m.low_bits >= 64 ? n : (n & ((1ull << m.low_bits) - 1));
+    return ((z >> m.rb_shift) << m.low_bits) | low;
+}
+
+inline OutMap make_outmap(double2* out, unsigned N, unsigned run_bits, int runs) {
+    return OutMap{out, N - run_bits, 2 * (N - run_bits), runs};
+}
+
 // ---- mbarrier / bulk-copy (TMA engine) PTX ----
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {

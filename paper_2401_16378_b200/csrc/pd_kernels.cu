@@ -96,20 +96,6 @@ static K2Geometry k2_geometry(unsigned N, unsigned K, uint64_t x_count) {
     return g;
 }
 
-struct RunOut {
-    double2* ptr[kMaxRuns];
-};
-
-// select a run pointer with constant indices only (a dynamic index into the
-// parameter struct would force a local-memory copy of it)
-__device__ __forceinline__ double2* run_ptr(const RunOut& runs, unsigned run) {
-    double2* p = runs.ptr[0];
-#pragma unroll
-    for (unsigned r = 1; r < kMaxRuns; ++r)
-        if (run == r) p = runs.ptr[r];
-    return p;
-}
-
 template <int K, bool ODD>
 __device__ __forceinline__ void gray_block(const double2* __restrict__ blk, unsigned sgn,
                                            double (&ar)[1 << K], double (&ai)[1 << K]) {
@@ -145,8 +131,7 @@ struct K2Params {
     unsigned c_begin, c_end;
     const double2* part_in;    // raw sums S[(x - x0) 2^N + z], or null
     double2* part_out;         // raw sums out, or null for coefficients
-    unsigned run_bits;
-    RunOut runs;
+    OutMap map;
     double scale;
 };
 
@@ -255,20 +240,16 @@ __global__ void __launch_bounds__(kK2Threads, 2) gray_xmask_kernel(const K2Param
         for (int j = 0; j < (1 << K); ++j) dst[j] = make_double2(ar[j], ai[j]);
         return;
     }
-    const unsigned low_bits = 2 * (N - P.run_bits);
-    const uint64_t low_mask = (low_bits >= 64) ? ~0ull : ((1ull << low_bits) - 1);
 #pragma unroll
     for (int zl = 0; zl < (1 << K); ++zl) {
         const uint64_t z = (zh << K) | static_cast<uint64_t>(zl);
         const unsigned ph = (3u * static_cast<unsigned>(__popcll(x & z))) & 3u;
-        const uint64_t n = tensor_number(x, z);
-        const unsigned run = static_cast<unsigned>(z >> (N - P.run_bits));
-        run_ptr(P.runs, run)[n & low_mask] = apply_phase(ph, ar[zl], ai[zl], P.scale);
+        P.map.out[out_index(P.map, tensor_number(x, z), z)] = apply_phase(ph, ar[zl], ai[zl], P.scale);
     }
 }
 
 template <int K>
-static cudaError_t launch_gray(const K2Params& P0, unsigned run_bits, cudaStream_t stream) {
+static cudaError_t launch_gray(const K2Params& P0, cudaStream_t stream) {
     const K2Geometry g = k2_geometry(P0.N, K, P0.x_count);
     static std::atomic<uint64_t> attr_set{0};  // per instantiation, one bit per device
     int dev = 0;
@@ -290,7 +271,6 @@ static cudaError_t launch_gray(const K2Params& P0, unsigned run_bits, cudaStream
     P.ci_log = g.ci_log;
     if (P.c_end == 0 || P.c_end > g.nchunks) P.c_end = g.nchunks;
     if (P.c_begin >= P.c_end) return cudaErrorInvalidValue;
-    P.run_bits = run_bits;
     P.scale = 1.0 / static_cast<double>(1ull << P.N);
     const bool seg = P.c_begin != 0 || P.c_end != g.nchunks || P.part_in || P.part_out;
     if (seg)
@@ -302,7 +282,7 @@ static cudaError_t launch_gray(const K2Params& P0, unsigned run_bits, cudaStream
 
 cudaError_t launch_gray_segment(const double2* diag, unsigned N, uint64_t x0, uint64_t x_count,
                                 unsigned c_begin, unsigned c_end, const double2* part_in,
-                                double2* part_out, unsigned run_bits, double2* const* run_out,
+                                double2* part_out, unsigned run_bits, double2* out, int layout,
                                 cudaStream_t stream) {
     K2Params P{};
     P.diag = diag;
@@ -313,19 +293,18 @@ cudaError_t launch_gray_segment(const double2* diag, unsigned N, uint64_t x0, ui
     P.c_end = c_end;
     P.part_in = part_in;
     P.part_out = part_out;
-    if (run_out != nullptr)
-        for (unsigned r = 0; r < (1u << run_bits); ++r) P.runs.ptr[r] = run_out[r];
+    P.map = make_outmap(out, N, run_bits, layout);
     switch (N < 4 ? N : 4) {
-        case 1: return launch_gray<1>(P, run_bits, stream);
-        case 2: return launch_gray<2>(P, run_bits, stream);
-        case 3: return launch_gray<3>(P, run_bits, stream);
-        default: return launch_gray<4>(P, run_bits, stream);
+        case 1: return launch_gray<1>(P, stream);
+        case 2: return launch_gray<2>(P, stream);
+        case 3: return launch_gray<3>(P, stream);
+        default: return launch_gray<4>(P, stream);
     }
 }
 
 cudaError_t launch_gray_xmask(const double2* diag, unsigned N, uint64_t x0, uint64_t x_count,
-                              unsigned run_bits, double2* const* run_out, cudaStream_t stream) {
-    return launch_gray_segment(diag, N, x0, x_count, 0, 0, nullptr, nullptr, run_bits, run_out,
+                              unsigned run_bits, double2* out, int layout, cudaStream_t stream) {
+    return launch_gray_segment(diag, N, x0, x_count, 0, 0, nullptr, nullptr, run_bits, out, layout,
                                stream);
 }
 

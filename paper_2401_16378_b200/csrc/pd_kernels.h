@@ -8,8 +8,7 @@
 
 namespace pdb {
 
-constexpr unsigned kMaxRunBits = 3;  // up to 8 X-mask shards (one 8xB200 box)
-constexpr unsigned kMaxRuns = 1u << kMaxRunBits;
+constexpr unsigned kMaxRunBits = 8;  // run bits of the RUNS output layout (shards x sub-blocks)
 
 extern std::atomic<uint64_t> g_launches;
 
@@ -25,24 +24,24 @@ cudaError_t launch_diag_gather_cols(const double2* G, unsigned N, uint64_t x0, u
 // part_in (null: from zero) and storing raw sums to part_out (null: finished coefficients)
 cudaError_t launch_gray_segment(const double2* diag, unsigned N, uint64_t x0, uint64_t x_count,
                                 unsigned c_begin, unsigned c_end, const double2* part_in,
-                                double2* part_out, unsigned run_bits, double2* const* run_out,
+                                double2* part_out, unsigned run_bits, double2* out, int layout,
                                 cudaStream_t stream);
 unsigned gray_xmask_chunks(unsigned N);  // walk chunks per diagonal (1 for N < 12)
 
-// K2: Gray-code sums for the X-masks [x0, x0 + x_count); run addressing as in pd_api.h
+// K2: Gray-code sums for the X-masks [x0, x0 + x_count); output layout as in pd_api.h
 cudaError_t launch_gray_xmask(const double2* diag, unsigned N, uint64_t x0, uint64_t x_count,
-                              unsigned run_bits, double2* const* run_out, cudaStream_t stream);
+                              unsigned run_bits, double2* out, int layout, cudaStream_t stream);
 uint64_t gray_xmask_grid(unsigned N, uint64_t x_count);
 
 // K4: fast Walsh-Hadamard path over the same diagonals (separately reported)
 cudaError_t launch_wht_xmask(const double2* diag, unsigned N, uint64_t x0, uint64_t x_count,
-                             unsigned run_bits, double2* const* run_out, cudaStream_t stream);
+                             unsigned run_bits, double2* out, int layout, cudaStream_t stream);
 
 // K4 fused two-pass WHT straight from G for X-masks [x0, x0 + x_count) (N in [8,16],
 // x_count >= 32); scratch holds x_count * 2^N complex128 (the half-transformed diagonals)
 bool wht_fused_ok(unsigned N, uint64_t x_count);
 cudaError_t launch_wht_from_matrix(const double2* G, unsigned N, uint64_t x0, uint64_t x_count,
-                                   double2* scratch, unsigned run_bits, double2* const* run_out,
+                                   double2* scratch, unsigned run_bits, double2* out, int layout,
                                    cudaStream_t stream);
 
 // in-place unnormalised Walsh-Hadamard transform of x_count rows of 2^N (N <= 16)

@@ -26,28 +26,16 @@ namespace {
 constexpr int kWhtThreads = 256;
 constexpr unsigned kWhtMaxL = 12;
 
-struct Runs {
-    double2* ptr[kMaxRuns];
-};
 
-__device__ __forceinline__ void store_coeff(const Runs& runs, unsigned N, unsigned run_bits,
-                                            uint64_t x, uint64_t z, double sr, double si,
-                                            double scale) {
+__device__ __forceinline__ void store_coeff(const OutMap& map, uint64_t x, uint64_t z, double sr,
+                                            double si, double scale) {
     const unsigned ph = (3u * static_cast<unsigned>(__popcll(x & z))) & 3u;
-    const uint64_t n = tensor_number(x, z);
-    const unsigned low_bits = 2 * (N - run_bits);
-    const uint64_t low_mask = (low_bits >= 64) ? ~0ull : ((1ull << low_bits) - 1);
-    const unsigned run = static_cast<unsigned>(z >> (N - run_bits));
-    double2* p = runs.ptr[0];
-#pragma unroll
-    for (unsigned r = 1; r < kMaxRuns; ++r)
-        if (run == r) p = runs.ptr[r];
-    p[n & low_mask] = apply_phase(ph, sr, si, scale);
+    __stcs(&map.out[out_index(map, tensor_number(x, z), z)], apply_phase(ph, sr, si, scale));
 }
 
 __global__ void __launch_bounds__(kWhtThreads)
     wht_rows_kernel(double2* __restrict__ diag, unsigned N, unsigned L, uint64_t x0,
-                    unsigned run_bits, Runs runs, double scale, int final_pass) {
+                    OutMap map, double scale, int final_pass) {
     // final_pass != 0: emit coefficients; otherwise write the transformed row back
     extern __shared__ __align__(16) double2 row[];
     const uint64_t dim = 1ull << N;
@@ -71,7 +59,7 @@ __global__ void __launch_bounds__(kWhtThreads)
     if (final_pass) {
         const uint64_t x = x0 + xl;
         for (unsigned j = threadIdx.x; j < len; j += kWhtThreads)
-            store_coeff(runs, N, run_bits, x, j, row[j].x, row[j].y, scale);
+            store_coeff(map, x, j, row[j].x, row[j].y, scale);
     } else {
         for (unsigned j = threadIdx.x; j < len; j += kWhtThreads) src[j] = row[j];
     }
@@ -80,7 +68,7 @@ __global__ void __launch_bounds__(kWhtThreads)
 template <int R>  // R = N - L high bits
 __global__ void __launch_bounds__(kWhtThreads)
     wht_cols_kernel(double2* __restrict__ diag, unsigned N, unsigned L, uint64_t x0,
-                    uint64_t x_count, unsigned run_bits, Runs runs, double scale, int emit) {
+                    uint64_t x_count, OutMap map, double scale, int emit) {
     const uint64_t t = static_cast<uint64_t>(blockIdx.x) * kWhtThreads + threadIdx.x;
     const uint64_t cols = 1ull << L;
     if (t >= x_count * cols) return;
@@ -107,8 +95,7 @@ __global__ void __launch_bounds__(kWhtThreads)
     const uint64_t x = x0 + xl;
 #pragma unroll
     for (int r = 0; r < (1 << R); ++r)
-        store_coeff(runs, N, run_bits, x, (static_cast<uint64_t>(r) << L) | il, v[r].x, v[r].y,
-                    scale);
+        store_coeff(map, x, (static_cast<uint64_t>(r) << L) | il, v[r].x, v[r].y, scale);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -203,7 +190,7 @@ __global__ void __launch_bounds__(kWhtThreads, 2)
 template <int HB, int XPC_LOG>
 __global__ void __launch_bounds__(kWhtThreads, 2)
     wht_hi_out_kernel(const double2* __restrict__ dprime, unsigned N, uint64_t x0,
-                      unsigned run_bits, Runs runs, double scale) {
+                      OutMap map, double scale) {
     extern __shared__ __align__(16) double2 s2[];
     constexpr unsigned L = HB + 3;                            // row = (hi, j), j = 3 low bits
     constexpr unsigned kRow = (1u << L) + ((1u << L) >> 4);
@@ -241,10 +228,7 @@ __global__ void __launch_bounds__(kWhtThreads, 2)
         else wht_round<1>(s2, L, kRow, 1u << XPC_LOG, b);
         __syncthreads();
     }
-    // per-thread constants of the output mapping: e = (hi, xl, j) with j fastest
-    const uint64_t zlow = (jb << 3);
-    const unsigned low_bits = 2 * (N - run_bits);
-    const uint64_t low_mask = (low_bits >= 64) ? ~0ull : ((1ull << low_bits) - 1);
+    // output mapping: e = (hi, xl, j) with j fastest
 #pragma unroll
     for (int it = 0; it < kIters; ++it) {
         const unsigned e = threadIdx.x + it * kWhtThreads;
@@ -252,15 +236,8 @@ __global__ void __launch_bounds__(kWhtThreads, 2)
             const unsigned j = e & 7, xl = (e >> 3) & ((1u << XPC_LOG) - 1), hi = e >> (3 + XPC_LOG);
             const double2 w = s2[xl * kRow + pad16((hi << 3) | j)];
             const uint64_t x = x0 + (xq << XPC_LOG) + xl;
-            const uint64_t z = (static_cast<uint64_t>(hi) << kLoBits) | zlow | j;
-            const unsigned ph = (3u * static_cast<unsigned>(__popcll(x & z))) & 3u;
-            const uint64_t n = tensor_number(x, z);
-            const unsigned run = static_cast<unsigned>(z >> (N - run_bits));
-            double2* p = runs.ptr[0];
-#pragma unroll
-            for (unsigned r = 1; r < kMaxRuns; ++r)
-                if (run == r) p = runs.ptr[r];
-            __stcs(&p[n & low_mask], apply_phase(ph, w.x, w.y, scale));
+            const uint64_t z = (static_cast<uint64_t>(hi) << kLoBits) | (jb << 3) | j;
+            store_coeff(map, x, z, w.x, w.y, scale);
         }
     }
 }
@@ -272,8 +249,8 @@ __global__ void __launch_bounds__(kWhtThreads, 2)
 // 2 shared-memory accesses and 1 barrier per element (the generic kernel above needs 6 and 3).
 template <int HB>
 __global__ void __launch_bounds__(kWhtThreads, 2)
-    wht_hi_reg_kernel(const double2* __restrict__ dprime, unsigned N, uint64_t x0,
-                      unsigned run_bits, Runs runs, double scale) {
+    wht_hi_reg_kernel(const double2* __restrict__ dprime, unsigned N, uint64_t x0, OutMap map,
+                      double scale) {
     static_assert(HB >= 4 && HB <= 8, "16 elements per thread in both rounds");
     extern __shared__ __align__(16) double2 s2[];             // [2^HB][COLS]
     constexpr int RB = HB - 4;                                 // bits of round B
@@ -303,8 +280,6 @@ __global__ void __launch_bounds__(kWhtThreads, 2)
         for (int r = 0; r < 16; ++r) s2[((a << 4) | r) * COLS + col] = v[r];
     }
     __syncthreads();
-    const unsigned low_bits = 2 * (N - run_bits);
-    const uint64_t low_mask = (low_bits >= 64) ? ~0ull : ((1ull << low_bits) - 1);
 #pragma unroll
     for (int q = 0; q < PAIRS; ++q) {
         const unsigned p = threadIdx.x + q * kWhtThreads;
@@ -325,14 +300,7 @@ __global__ void __launch_bounds__(kWhtThreads, 2)
 #pragma unroll
         for (int h = 0; h < (1 << RB); ++h) {
             const uint64_t z = (static_cast<uint64_t>((h << 4) | hlo) << kLoBits) | (jb << 3) | (col & 7);
-            const unsigned ph = (3u * static_cast<unsigned>(__popcll(x & z))) & 3u;
-            const uint64_t n = tensor_number(x, z);
-            const unsigned run = static_cast<unsigned>(z >> (N - run_bits));
-            double2* dst = runs.ptr[0];
-#pragma unroll
-            for (unsigned r = 1; r < kMaxRuns; ++r)
-                if (run == r) dst = runs.ptr[r];
-            __stcs(&dst[n & low_mask], apply_phase(ph, v[h].x, v[h].y, scale));
+            store_coeff(map, x, z, v[h].x, v[h].y, scale);
         }
     }
 }
@@ -342,7 +310,7 @@ __global__ void __launch_bounds__(kWhtThreads, 2)
 // shared driver: rows pass, then (N > 12) the column pass; emit != 0 writes
 // coefficients through `runs`, emit == 0 leaves the transform in place in `buf`
 static cudaError_t wht_passes(double2* buf, unsigned N, uint64_t x0, uint64_t x_count,
-                              unsigned run_bits, const Runs& runs, int emit, cudaStream_t stream) {
+                              const OutMap& map, int emit, cudaStream_t stream) {
     const unsigned L = N < kWhtMaxL ? N : kWhtMaxL;
     const unsigned R = N - L;
     if (R > 4) return cudaErrorInvalidValue;  // N <= 16
@@ -358,32 +326,31 @@ static cudaError_t wht_passes(double2* buf, unsigned N, uint64_t x0, uint64_t x_
     }
     const uint64_t grid1 = x_count << R;
     wht_rows_kernel<<<static_cast<unsigned>(grid1), kWhtThreads, sizeof(double2) << L, stream>>>(
-        buf, N, L, x0, run_bits, runs, scale, emit && R == 0);
+        buf, N, L, x0, map, scale, emit && R == 0);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || R == 0) return e;
     const unsigned grid2 = static_cast<unsigned>(((x_count << L) + kWhtThreads - 1) / kWhtThreads);
     switch (R) {
-        case 1: wht_cols_kernel<1><<<grid2, kWhtThreads, 0, stream>>>(buf, N, L, x0, x_count, run_bits, runs, scale, emit); break;
-        case 2: wht_cols_kernel<2><<<grid2, kWhtThreads, 0, stream>>>(buf, N, L, x0, x_count, run_bits, runs, scale, emit); break;
-        case 3: wht_cols_kernel<3><<<grid2, kWhtThreads, 0, stream>>>(buf, N, L, x0, x_count, run_bits, runs, scale, emit); break;
-        default: wht_cols_kernel<4><<<grid2, kWhtThreads, 0, stream>>>(buf, N, L, x0, x_count, run_bits, runs, scale, emit); break;
+        case 1: wht_cols_kernel<1><<<grid2, kWhtThreads, 0, stream>>>(buf, N, L, x0, x_count, map, scale, emit); break;
+        case 2: wht_cols_kernel<2><<<grid2, kWhtThreads, 0, stream>>>(buf, N, L, x0, x_count, map, scale, emit); break;
+        case 3: wht_cols_kernel<3><<<grid2, kWhtThreads, 0, stream>>>(buf, N, L, x0, x_count, map, scale, emit); break;
+        default: wht_cols_kernel<4><<<grid2, kWhtThreads, 0, stream>>>(buf, N, L, x0, x_count, map, scale, emit); break;
     }
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return cudaGetLastError();
 }
 
 cudaError_t launch_wht_xmask(const double2* diag_c, unsigned N, uint64_t x0, uint64_t x_count,
-                             unsigned run_bits, double2* const* run_out, cudaStream_t stream) {
+                             unsigned run_bits, double2* out, int layout, cudaStream_t stream) {
     // the passes rewrite the diagonal rows in place (they are scratch owned by the caller)
-    Runs runs{};
-    for (unsigned r = 0; r < (1u << run_bits); ++r) runs.ptr[r] = run_out[r];
-    return wht_passes(const_cast<double2*>(diag_c), N, x0, x_count, run_bits, runs, 1, stream);
+    return wht_passes(const_cast<double2*>(diag_c), N, x0, x_count,
+                      make_outmap(out, N, run_bits, layout), 1, stream);
 }
 
 // pass 2 dispatch: the register-round kernel for HB in [4, 8], the generic one otherwise
 static cudaError_t launch_pass2(const double2* scratch, unsigned N, uint64_t x0, uint64_t x_count,
-                                unsigned run_bits, const Runs& runs, cudaStream_t stream) {
+                                const OutMap& map, cudaStream_t stream) {
     const unsigned hb = N - kLoBits;
     if (hb < 4 || hb > 8 || x_count < (1ull << (9 - hb))) return cudaErrorNotSupported;
     const double scale = 1.0 / static_cast<double>(1ull << N);
@@ -394,7 +361,7 @@ static cudaError_t launch_pass2(const double2* scratch, unsigned N, uint64_t x0,
     do {                                                                                         \
         auto k = wht_hi_reg_kernel<HBV>;                                                         \
         e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);         \
-        if (e == cudaSuccess) k<<<grid, kWhtThreads, smem, stream>>>(scratch, N, x0, run_bits, runs, scale); \
+        if (e == cudaSuccess) k<<<grid, kWhtThreads, smem, stream>>>(scratch, N, x0, map, scale);                    \
     } while (0)
     switch (hb) {
         case 4: PD_REG(4); break;
@@ -412,10 +379,9 @@ static cudaError_t launch_pass2(const double2* scratch, unsigned N, uint64_t x0,
 bool wht_fused_ok(unsigned N, uint64_t x_count) { return N >= 8 && N <= 16 && x_count >= 32; }
 
 cudaError_t launch_wht_from_matrix(const double2* G, unsigned N, uint64_t x0, uint64_t x_count,
-                                   double2* scratch, unsigned run_bits, double2* const* run_out,
+                                   double2* scratch, unsigned run_bits, double2* out, int layout,
                                    cudaStream_t stream) {
-    Runs runs{};
-    for (unsigned r = 0; r < (1u << run_bits); ++r) runs.ptr[r] = run_out[r];
+    const OutMap map = make_outmap(out, N, run_bits, layout);
     static std::atomic<uint64_t> attr_set{0};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -430,7 +396,7 @@ cudaError_t launch_wht_from_matrix(const double2* G, unsigned N, uint64_t x0, ui
     g_launches.fetch_add(1, std::memory_order_relaxed);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    if (launch_pass2(scratch, N, x0, x_count, run_bits, runs, stream) == cudaSuccess) {
+    if (launch_pass2(scratch, N, x0, x_count, map, stream) == cudaSuccess) {
         g_launches.fetch_add(1, std::memory_order_relaxed);
         return cudaGetLastError();
     }
@@ -447,7 +413,7 @@ cudaError_t launch_wht_from_matrix(const double2* G, unsigned N, uint64_t x0, ui
         auto k = wht_hi_out_kernel<HBV, XL>;                                                  \
         e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kP1Smem);    \
         if (e == cudaSuccess)                                                                 \
-            k<<<grid2, kWhtThreads, smem, stream>>>(scratch, N, x0, run_bits, runs, scale);   \
+            k<<<grid2, kWhtThreads, smem, stream>>>(scratch, N, x0, map, scale);             \
     } while (0)
     switch (hb * 4 + xpc_log) {
         case 1 * 4 + 2: PD_HI(1, 2); break;
@@ -468,8 +434,7 @@ cudaError_t launch_wht_from_matrix(const double2* G, unsigned N, uint64_t x0, ui
 }
 
 cudaError_t launch_wht_inplace(double2* rows, unsigned N, uint64_t x_count, cudaStream_t stream) {
-    Runs runs{};
-    return wht_passes(rows, N, 0, x_count, 0, runs, 0, stream);
+    return wht_passes(rows, N, 0, x_count, make_outmap(nullptr, N, 0, 0), 0, stream);
 }
 
 }  // namespace pdb

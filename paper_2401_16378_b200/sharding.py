@@ -29,8 +29,10 @@ import torch.distributed as dist
 
 from . import _paulidecomp as _ext
 
-# compute(G, x0, x_count, run_bits, run_views, diag) fills run_views (complex128 views)
-ShardCompute = Callable[[torch.Tensor, int, int, int, List[torch.Tensor], Optional[torch.Tensor]], None]
+# compute(G, x0, x_count, run_bits, dst, layout, diag) writes the coefficients of the X-mask
+# block into dst: "global" = the reference-ordered array of all 4^N (rank 0, in place),
+# "runs" = the block's 2^run_bits runs packed back to back (pd_layout, include/pd_api.h)
+ShardCompute = Callable[[torch.Tensor, int, int, int, torch.Tensor, str, Optional[torch.Tensor]], None]
 
 
 def run_offset(num_qubits: int, run_bits: int, shard: int, run: int) -> int:
@@ -65,11 +67,11 @@ def device_compute(path: str = "gray") -> ShardCompute:
     """One shard's coefficients straight from G on the current CUDA stream:
     K1 + K2 (gray) or the fused two-pass WHT (wht), via pd_shard_coeffs_device."""
 
-    def compute(G, x0, x_count, run_bits, runs, diag):
+    def compute(G, x0, x_count, run_bits, dst, layout, diag):
         N = int(G.shape[0]).bit_length() - 1
         stream = torch.cuda.current_stream(G.device).cuda_stream
-        _ext.device.shard_coeffs(N, G.data_ptr(), x0, x_count, run_bits,
-                                 [r.data_ptr() for r in runs], diag.data_ptr(), path, stream)
+        _ext.device.shard_coeffs(N, G.data_ptr(), x0, x_count, run_bits, dst.data_ptr(), layout,
+                                 diag.data_ptr(), path, stream)
 
     return compute
 
@@ -96,10 +98,9 @@ class ShardedDecomposer:
         if p.rank != 0:
             self.local = torch.empty(p.run_len << p.run_bits, dtype=torch.complex128, device=device)
 
-    def run_views(self, out: Optional[torch.Tensor]) -> List[torch.Tensor]:
+    def run_views(self) -> List[torch.Tensor]:
+        """This (non-zero) rank's packed runs, in Z-mask top-bit order."""
         p = self.plan
-        if p.rank == 0:
-            return [out[o:o + p.run_len] for o in p.offsets()]
         return [self.local[r * p.run_len:(r + 1) * p.run_len] for r in range(1 << p.run_bits)]
 
     def broadcast(self, G: torch.Tensor) -> None:
@@ -108,7 +109,10 @@ class ShardedDecomposer:
 
     def compute_local(self, G: torch.Tensor, out: Optional[torch.Tensor]) -> None:
         p = self.plan
-        self.compute(G, p.x0, p.x_count, p.run_bits, self.run_views(out), self.diag)
+        if p.rank == 0:
+            self.compute(G, p.x0, p.x_count, p.run_bits, out, "global", self.diag)
+        else:
+            self.compute(G, p.x0, p.x_count, p.run_bits, self.local, "runs", self.diag)
 
     def gather(self, out: Optional[torch.Tensor]) -> None:
         p = self.plan
@@ -120,9 +124,8 @@ class ShardedDecomposer:
                 for r, o in enumerate(p.offsets(src)):
                     ops.append(dist.P2POp(dist.irecv, out[o:o + p.run_len], src, group=self.group))
         else:
-            for r in range(1 << p.run_bits):
-                ops.append(dist.P2POp(dist.isend, self.local[r * p.run_len:(r + 1) * p.run_len], 0,
-                                      group=self.group))
+            for run in self.run_views():
+                ops.append(dist.P2POp(dist.isend, run, 0, group=self.group))
         for req in dist.batch_isend_irecv(ops):
             req.wait()
 

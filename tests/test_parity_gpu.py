@@ -158,36 +158,72 @@ def test_recompose_round_trip(pd, cuda, port):
     np.testing.assert_allclose(pd.recompose(c), port.recompose(c), rtol=0, atol=1e-12)
 
 
+def _scatter_runs(pd, out, packed, nq, p, shard):
+    """place a block's packed runs (PD_LAYOUT_RUNS) at their pd_run_offset in `out`"""
+    rl = 4 ** (nq - p)
+    for r in range(2**p):
+        o = pd.device.run_offset(nq, p, shard, r)
+        out[o:o + rl] = packed[r * rl:(r + 1) * rl]
+
+
 def test_sharded_runs_assemble_full_array(pd, cuda):
-    # the multi-GPU addressing, emulated shard by shard on one GPU (no collectives)
+    # the multi-GPU addressing, emulated shard by shard on one GPU (no collectives):
+    # GLOBAL layout writes in place, RUNS layout packs each block (up to 2^8 blocks)
     import torch
     nq = 9
     g = torch.from_numpy(normal_matrix(np.random.default_rng(8), nq)).to(cuda)
     full = torch.empty(4**nq, dtype=torch.complex128, device=cuda)
     scratch = torch.empty(4**nq, dtype=torch.complex128, device=cuda)
     pd.device.decompose(nq, g.data_ptr(), full.data_ptr(), scratch.data_ptr(), "gray", 0)
-    for p in (1, 2, 3):
-        out = torch.zeros_like(full)
+    for p in (1, 2, 3, 5, 8):
         xc = 2 ** (nq - p)
-        diag = torch.empty(xc * 2**nq, dtype=torch.complex128, device=cuda)
+        diag = torch.empty(max(xc, 32) * 2**nq, dtype=torch.complex128, device=cuda)
+        packed = torch.empty(4**nq >> p, dtype=torch.complex128, device=cuda)
+        out = torch.zeros_like(full)
+        out_runs = torch.zeros_like(full)
         for shard in range(2**p):
             pd.device.diag_gather(nq, g.data_ptr(), shard * xc, xc, diag.data_ptr(), 0)
-            runs = [out[pd.device.run_offset(nq, p, shard, r):].data_ptr() for r in range(2**p)]
-            pd.device.xmask_coeffs(nq, diag.data_ptr(), shard * xc, xc, p, runs, "gray", 0)
+            pd.device.xmask_coeffs(nq, diag.data_ptr(), shard * xc, xc, p, out.data_ptr(),
+                                   "global", "gray", 0)
+            pd.device.xmask_coeffs(nq, diag.data_ptr(), shard * xc, xc, p, packed.data_ptr(),
+                                   "runs", "gray", 0)
+            _scatter_runs(pd, out_runs, packed, nq, p, shard)
         torch.cuda.synchronize()
         assert torch.equal(out, full), p
-        # the one-call shard entry point, both paths (WHT: fused two-pass from G)
+        assert torch.equal(out_runs, full), p
+        # the one-call shard entry point, both paths (WHT: fused two-pass from G when x_count >= 32)
         for path in ("gray", "wht"):
             out2 = torch.zeros_like(full)
+            out3 = torch.zeros_like(full)
             for shard in range(2**p):
-                runs = [out2[pd.device.run_offset(nq, p, shard, r):].data_ptr() for r in range(2**p)]
-                pd.device.shard_coeffs(nq, g.data_ptr(), shard * xc, xc, p, runs, diag.data_ptr(), path, 0)
+                pd.device.shard_coeffs(nq, g.data_ptr(), shard * xc, xc, p, out2.data_ptr(),
+                                       "global", diag.data_ptr(), path, 0)
+                pd.device.shard_coeffs(nq, g.data_ptr(), shard * xc, xc, p, packed.data_ptr(),
+                                       "runs", diag.data_ptr(), path, 0)
+                _scatter_runs(pd, out3, packed, nq, p, shard)
             torch.cuda.synchronize()
-            if path == "gray":
-                assert torch.equal(out2, full), (p, path)
-            else:
-                err = float(torch.max(torch.abs(out2 - full)) / torch.max(torch.abs(full)))
-                assert err <= TOL, (p, err)
+            for o in (out2, out3):
+                if path == "gray":
+                    assert torch.equal(o, full), (p, path)
+                else:
+                    err = float(torch.max(torch.abs(o - full)) / torch.max(torch.abs(full)))
+                    assert err <= TOL, (p, err)
+
+
+def test_xmask_range_validation(pd, cuda):
+    import torch
+    nq = 6
+    g = torch.zeros((64, 64), dtype=torch.complex128, device=cuda)
+    out = torch.empty(4**nq, dtype=torch.complex128, device=cuda)
+    diag = torch.empty(64 * 64, dtype=torch.complex128, device=cuda)
+    with pytest.raises(ValueError):   # spans two blocks of 2^(N-p)
+        pd.device.shard_coeffs(nq, g.data_ptr(), 0, 64, 1, out.data_ptr(), "runs", diag.data_ptr())
+    with pytest.raises(ValueError):   # run_bits > 8
+        pd.device.shard_coeffs(nq, g.data_ptr(), 0, 1, 9, out.data_ptr(), "runs", diag.data_ptr())
+    with pytest.raises(ValueError):   # misaligned range
+        pd.device.shard_coeffs(nq, g.data_ptr(), 3, 2, 0, out.data_ptr(), "global", diag.data_ptr())
+    with pytest.raises(ValueError):
+        pd.device.shard_coeffs(nq, g.data_ptr(), 0, 64, 0, out.data_ptr(), "bogus", diag.data_ptr())
 
 
 def test_n14_config5(pd, cuda, port, golden):

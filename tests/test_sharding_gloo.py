@@ -22,7 +22,7 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-def _oracle_compute(G, x0, x_count, run_bits, runs, diag):
+def _oracle_compute(G, x0, x_count, run_bits, dst, layout, diag):
     import sys
     sys.path.insert(0, ROOT)
     from oracle import oracle as O
@@ -33,11 +33,13 @@ def _oracle_compute(G, x0, x_count, run_bits, runs, diag):
     for x in range(x0, x0 + x_count):
         ns = O.xz_to_n(np.uint64(x), z, nq)
         vals = O.port().coeff_batch(g, ns, threads=1)
+        if layout == "global":
+            dst[torch.from_numpy(ns.astype(np.int64))] = torch.from_numpy(vals)
+            continue
+        # packed runs: run r (Z-mask top bits) at r * 4^(N-p), n's low 2(N-p) bits inside it
         rsel = (z >> np.uint64(nq - run_bits)).astype(np.int64)
         local = (ns & np.uint64((1 << low) - 1)).astype(np.int64)
-        for r in range(1 << run_bits):
-            m = rsel == r
-            runs[r][torch.from_numpy(local[m])] = torch.from_numpy(vals[m])
+        dst[torch.from_numpy((rsel << low) | local)] = torch.from_numpy(vals)
 
 
 def _worker(rank, world, port, nq, result_path):
