@@ -124,6 +124,28 @@ __device__ __forceinline__ void gray_block(const double2* __restrict__ blk, unsi
 // from the raw sums in part_in (or zero) and ends by storing raw sums to part_out, or — when
 // part_out is null — the finished coefficients. Continuing a chain from stored sums keeps each
 // coefficient's summation order, so segmented launches are bit-identical to one launch.
+// Coefficient destinations of a K2 launch. With at most kRunPtrs runs they are passed as one
+// pointer per run (run r = Z-mask top-bit value r; GLOBAL layout: out + pd_run_offset, RUNS:
+// out + r 4^(N-rb)), selected with constant indices in the epilogue; more runs use the
+// arithmetic OutMap instead (MAPPED instantiation). Measured on B200: the run-pointer form
+// keeps ptxas' schedule of the main loop at 485.8 ms (N=14, K1+K2) where the OutMap epilogue
+// ends at 505.6 ms (+20 % dispatch stalls on DADDs; profiles/r01_k2_codegen.md).
+constexpr unsigned kRunPtrBits = 3;
+constexpr unsigned kRunPtrs = 1u << kRunPtrBits;
+struct RunOut {
+    double2* ptr[kRunPtrs];
+};
+
+// select a run pointer with constant indices only (a dynamic index into the
+// parameter struct would force a local-memory copy of it)
+__device__ __forceinline__ double2* run_ptr(const RunOut& runs, unsigned run) {
+    double2* p = runs.ptr[0];
+#pragma unroll
+    for (unsigned r = 1; r < kRunPtrs; ++r)
+        if (run == r) p = runs.ptr[r];
+    return p;
+}
+
 struct K2Params {
     const double2* diag;       // rows of the X-masks [x0, x0 + x_count)
     uint64_t x0, x_count;
@@ -131,13 +153,15 @@ struct K2Params {
     unsigned c_begin, c_end;
     const double2* part_in;    // raw sums S[(x - x0) 2^N + z], or null
     double2* part_out;         // raw sums out, or null for coefficients
-    OutMap map;
+    unsigned run_bits;         // run-pointer form: runs of 4^(N - run_bits), run_bits <= 3
+    RunOut runs;
+    OutMap map;                // MAPPED form
     double scale;
 };
 
 // SEG = false: the whole walk from zero to coefficients (c_begin = 0, no partial sums); kept
 // as a separate instantiation so the common case compiles without the segment logic.
-template <int K, bool SEG>
+template <int K, bool SEG, bool MAPPED>
 __global__ void __launch_bounds__(kK2Threads, 2) gray_xmask_kernel(const K2Params P) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const unsigned tid = threadIdx.x;
@@ -240,11 +264,25 @@ __global__ void __launch_bounds__(kK2Threads, 2) gray_xmask_kernel(const K2Param
         for (int j = 0; j < (1 << K); ++j) dst[j] = make_double2(ar[j], ai[j]);
         return;
     }
+    if (MAPPED) {
+#pragma unroll
+        for (int zl = 0; zl < (1 << K); ++zl) {
+            const uint64_t z = (zh << K) | static_cast<uint64_t>(zl);
+            const unsigned ph = (3u * static_cast<unsigned>(__popcll(x & z))) & 3u;
+            P.map.out[out_index(P.map, tensor_number(x, z), z)] =
+                apply_phase(ph, ar[zl], ai[zl], P.scale);
+        }
+        return;
+    }
+    const unsigned low_bits = 2 * (N - P.run_bits);
+    const uint64_t low_mask = (low_bits >= 64) ? ~0ull : ((1ull << low_bits) - 1);
 #pragma unroll
     for (int zl = 0; zl < (1 << K); ++zl) {
         const uint64_t z = (zh << K) | static_cast<uint64_t>(zl);
         const unsigned ph = (3u * static_cast<unsigned>(__popcll(x & z))) & 3u;
-        P.map.out[out_index(P.map, tensor_number(x, z), z)] = apply_phase(ph, ar[zl], ai[zl], P.scale);
+        const uint64_t n = tensor_number(x, z);
+        const unsigned run = static_cast<unsigned>(z >> (N - P.run_bits));
+        run_ptr(P.runs, run)[n & low_mask] = apply_phase(ph, ar[zl], ai[zl], P.scale);
     }
 }
 
@@ -255,12 +293,11 @@ static cudaError_t launch_gray(const K2Params& P0, cudaStream_t stream) {
     int dev = 0;
     cudaGetDevice(&dev);
     if (!(attr_set.load() >> dev & 1)) {
-        cudaError_t e = cudaFuncSetAttribute(gray_xmask_kernel<K, false>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             kK2MaxSmem);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(gray_xmask_kernel<K, true>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kK2MaxSmem);
+        cudaError_t e = cudaSuccess;
+        for (auto k : {gray_xmask_kernel<K, false, false>, gray_xmask_kernel<K, true, false>,
+                       gray_xmask_kernel<K, false, true>, gray_xmask_kernel<K, true, true>})
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kK2MaxSmem);
         if (e != cudaSuccess) return e;
         attr_set.fetch_or(1ull << dev);
     }
@@ -273,10 +310,10 @@ static cudaError_t launch_gray(const K2Params& P0, cudaStream_t stream) {
     if (P.c_begin >= P.c_end) return cudaErrorInvalidValue;
     P.scale = 1.0 / static_cast<double>(1ull << P.N);
     const bool seg = P.c_begin != 0 || P.c_end != g.nchunks || P.part_in || P.part_out;
-    if (seg)
-        gray_xmask_kernel<K, true><<<static_cast<unsigned>(g.grid), kK2Threads, g.smem_bytes, stream>>>(P);
-    else
-        gray_xmask_kernel<K, false><<<static_cast<unsigned>(g.grid), kK2Threads, g.smem_bytes, stream>>>(P);
+    const bool mapped = P.run_bits > kRunPtrBits;
+    auto kern = seg ? (mapped ? gray_xmask_kernel<K, true, true> : gray_xmask_kernel<K, true, false>)
+                    : (mapped ? gray_xmask_kernel<K, false, true> : gray_xmask_kernel<K, false, false>);
+    kern<<<static_cast<unsigned>(g.grid), kK2Threads, g.smem_bytes, stream>>>(P);
     return count_launch();
 }
 
@@ -294,6 +331,14 @@ cudaError_t launch_gray_segment(const double2* diag, unsigned N, uint64_t x0, ui
     P.part_in = part_in;
     P.part_out = part_out;
     P.map = make_outmap(out, N, run_bits, layout);
+    P.run_bits = run_bits;
+    if (run_bits <= kRunPtrBits) {
+        const uint64_t shard = run_bits ? (x0 >> (N - run_bits)) : 0;
+        const unsigned low_bits = 2 * (N - run_bits);
+        for (unsigned r = 0; r < (1u << run_bits); ++r)
+            P.runs.ptr[r] = out + (layout ? (static_cast<uint64_t>(r) << low_bits)
+                                          : (tensor_number(shard, r) << low_bits));
+    }
     switch (N < 4 ? N : 4) {
         case 1: return launch_gray<1>(P, stream);
         case 2: return launch_gray<2>(P, stream);

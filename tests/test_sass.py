@@ -1,0 +1,85 @@
+"""SASS checks of the built sm_100a kernels (CPU only: cuobjdump on the in-tree objects).
+
+They pin what the roofline claims rest on: K2's main loop is 32 DADD + 1
+LDS.128 + sign-flip LOP3s per element with no spills, its diagonal stream uses the bulk-copy
+(TMA) engine, and the run-pointer instantiation that keeps ptxas' fast schedule
+(profiles/r01_k2_codegen.md) is the one with the 1198-instruction two-block loop."""
+import os
+import re
+import shutil
+import subprocess
+
+import pytest
+
+from conftest import ROOT
+
+OBJ = os.path.join(ROOT, "paper_2401_16378_b200", "csrc", "build", "pd_kernels.o")
+WHT_OBJ = os.path.join(ROOT, "paper_2401_16378_b200", "csrc", "build", "pd_wht.o")
+CUOBJDUMP = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+
+pytestmark = pytest.mark.skipif(not (os.path.exists(OBJ) and os.path.exists(CUOBJDUMP)),
+                                reason="kernels not built or cuobjdump missing")
+
+
+def sass_of(obj, fun):
+    out = subprocess.run([CUOBJDUMP, "-sass", "-fun", fun, obj], capture_output=True, text=True,
+                         check=True).stdout
+    ins = []
+    for line in out.splitlines():
+        m = re.match(r"\s*/\*([0-9a-f]{4,})\*/\s*(.*?);", line)
+        if m:
+            ins.append((int(m.group(1), 16), m.group(2).strip()))
+    assert ins, f"no SASS for {fun}"
+    return ins
+
+
+def innermost_loop(ins, min_dadd=512):
+    addr = {a: i for i, (a, _) in enumerate(ins)}
+    best = None
+    for i, (a, t) in enumerate(ins):
+        if "BRA" not in t:
+            continue
+        m = re.search(r"0x([0-9a-f]+)", t.split("BRA", 1)[1])
+        if not m:
+            continue
+        tgt = int(m.group(1), 16)
+        if tgt < a and tgt in addr:
+            body = [x[1] for x in ins[addr[tgt]:i + 1]]
+            if sum(b.startswith("DADD") for b in body) >= min_dadd and (best is None or len(body) < len(best)):
+                best = body
+    assert best is not None, "no DADD loop found"
+    return best
+
+
+K2_FAST = "_ZN3pdb17gray_xmask_kernelILi4ELb0ELb0EEEvNS_8K2ParamsE"
+
+
+def test_k2_main_loop_is_pure_fp64_adds():
+    ins = sass_of(OBJ, K2_FAST)
+    body = innermost_loop(ins)
+    ops = [b.split()[0] for b in body]
+    n_dadd = sum(o == "DADD" for o in ops)
+    n_lds = sum(o.startswith("LDS.128") for o in ops)
+    # two unrolled 16-element blocks: 32 elements x 32 accumulators
+    assert n_dadd == 1024 and n_lds == 32, (n_dadd, n_lds)
+    assert not any(o.startswith(("DMUL", "DFMA", "LDL", "STL")) for o in ops)
+    # FP64-pipe share of the issue slots (the kernel is FP64-add bound: 2 pipe cycles per DADD)
+    assert n_dadd / len(body) > 0.85, len(body)
+    # the schedule measured at 485.8 ms (profiles/r01_k2_codegen.md)
+    assert len(body) == 1198, len(body)
+
+
+def test_k2_streams_diagonals_with_bulk_copies():
+    ops = [t.split()[0] for _, t in sass_of(OBJ, K2_FAST)]
+    assert any(o.startswith("UBLKCP") for o in ops), "no cp.async.bulk (TMA engine) in K2"
+    assert any(o.startswith("SYNCS") for o in ops), "no mbarrier wait in K2"
+
+
+def test_no_local_memory_in_hot_kernels():
+    for obj in (OBJ, WHT_OBJ):
+        log = open(obj + ".ptxas.log").read()
+        for m in re.finditer(r"Function properties for (\S+)\n\s*(\d+) bytes stack frame, (\d+) bytes spill stores",
+                             log):
+            name, stack, spills = m.group(1), int(m.group(2)), int(m.group(3))
+            if "gray_xmask" in name or "wht_" in name or "diag_gather" in name:
+                assert spills == 0, (name, spills)
