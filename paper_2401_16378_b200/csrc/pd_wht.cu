@@ -14,6 +14,9 @@
 //           2^(N-L) rows and writes coefficients.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+#include <mutex>
+
 #include <cstdint>
 
 #include "pd_device.cuh"
@@ -149,6 +152,7 @@ __device__ __forceinline__ void wht_round(double2* s, unsigned L, unsigned row_s
 constexpr unsigned kP1Row = (1u << kLoBits) + ((1u << kLoBits) >> 4);  // 136 padded elements
 constexpr size_t kP1Smem = 32 * kP1Row * sizeof(double2);                // 69,632 B
 
+template <bool KEEP>  // KEEP: D' stays in L2 for pass 2 (chunked pipeline); else streaming stores
 __global__ void __launch_bounds__(kWhtThreads, 2)
     wht_gather_lo_kernel(const double2* __restrict__ G, unsigned N, uint64_t x0,
                          double2* __restrict__ dprime) {
@@ -182,7 +186,9 @@ __global__ void __launch_bounds__(kWhtThreads, 2)
     for (int it = 0; it < kIters; ++it) {
         const unsigned e = threadIdx.x + it * kWhtThreads;
         const unsigned row = e >> 7, il = e & 127;
-        __stcs(&dprime[((xb << 5) + row) * dim + (grp << kLoBits) + il], s1[row * kP1Row + pad16(il)]);
+        double2* dst = &dprime[((xb << 5) + row) * dim + (grp << kLoBits) + il];
+        if (KEEP) *dst = s1[row * kP1Row + pad16(il)];
+        else __stcs(dst, s1[row * kP1Row + pad16(il)]);
     }
 }
 
@@ -247,7 +253,7 @@ __global__ void __launch_bounds__(kWhtThreads, 2)
 // [0, 4); one shared-memory exchange; round B butterflies bits [4, HB) and writes the
 // coefficients from registers (a warp covers 32 consecutive (x_low, j) columns: two 256 B runs).
 // 2 shared-memory accesses and 1 barrier per element (the generic kernel above needs 6 and 3).
-template <int HB>
+template <int HB, bool DISCARD>  // DISCARD: drop D' lines from L2 once read (never written back)
 __global__ void __launch_bounds__(kWhtThreads, 2)
     wht_hi_reg_kernel(const double2* __restrict__ dprime, unsigned N, uint64_t x0, OutMap map,
                       double scale) {
@@ -276,6 +282,14 @@ __global__ void __launch_bounds__(kWhtThreads, 2)
                 v[k] = make_double2(p.x + q.x, p.y + q.y);
                 v[k + h] = make_double2(p.x - q.x, p.y - q.y);
             }
+        if (DISCARD && (col & 7) == 0) {
+            // every element of these 128 B lines has been consumed by this warp (the butterflies
+            // above read all 16 loads), and nothing reads D' again before pass 1 rewrites it
+#pragma unroll
+            for (int r = 0; r < 16; ++r)
+                asm volatile("discard.global.L2 [%0], 128;" ::"l"(src + (static_cast<uint64_t>((a << 4) | r) << kLoBits))
+                             : "memory");
+        }
 #pragma unroll
         for (int r = 0; r < 16; ++r) s2[((a << 4) | r) * COLS + col] = v[r];
     }
@@ -350,7 +364,7 @@ cudaError_t launch_wht_xmask(const double2* diag_c, unsigned N, uint64_t x0, uin
 
 // pass 2 dispatch: the register-round kernel for HB in [4, 8], the generic one otherwise
 static cudaError_t launch_pass2(const double2* scratch, unsigned N, uint64_t x0, uint64_t x_count,
-                                const OutMap& map, cudaStream_t stream) {
+                                const OutMap& map, bool discard, cudaStream_t stream) {
     const unsigned hb = N - kLoBits;
     if (hb < 4 || hb > 8 || x_count < (1ull << (9 - hb))) return cudaErrorNotSupported;
     const double scale = 1.0 / static_cast<double>(1ull << N);
@@ -359,7 +373,7 @@ static cudaError_t launch_pass2(const double2* scratch, unsigned N, uint64_t x0,
     cudaError_t e = cudaSuccess;
 #define PD_REG(HBV)                                                                              \
     do {                                                                                         \
-        auto k = wht_hi_reg_kernel<HBV>;                                                         \
+        auto k = discard ? wht_hi_reg_kernel<HBV, true> : wht_hi_reg_kernel<HBV, false>;      \
         e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);         \
         if (e == cudaSuccess) k<<<grid, kWhtThreads, smem, stream>>>(scratch, N, x0, map, scale);                    \
     } while (0)
@@ -378,25 +392,66 @@ static cudaError_t launch_pass2(const double2* scratch, unsigned N, uint64_t x0,
 
 bool wht_fused_ok(unsigned N, uint64_t x_count) { return N >= 8 && N <= 16 && x_count >= 32; }
 
-cudaError_t launch_wht_from_matrix(const double2* G, unsigned N, uint64_t x0, uint64_t x_count,
-                                   double2* scratch, unsigned run_bits, double2* out, int layout,
-                                   cudaStream_t stream) {
-    const OutMap map = make_outmap(out, N, run_bits, layout);
+// Chunked L2-resident pipeline. D' of a chunk of S X-masks (S 2^N x 16 B, ~32 MiB) is written
+// by pass 1 with default (L2-allocating) stores and read back by pass 2 before it leaves L2;
+// pass 2 then discards the lines (discard.global.L2), so D' never reaches DRAM and the HBM
+// traffic is the algorithmic 32 4^N B (read G, write coefficients). Chunks alternate between
+// two D' slots and two streams, so one chunk's pass 2 overlaps the next chunk's pass 1.
+namespace {
+struct WhtPipe {
+    cudaStream_t side[2] = {nullptr, nullptr};
+    cudaEvent_t fork = nullptr, join[2] = {nullptr, nullptr};
+    bool ok = false;
+};
+
+WhtPipe& wht_pipe(int dev) {
+    static WhtPipe pipes[64];
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lk(mu);
+    WhtPipe& p = pipes[dev & 63];
+    if (!p.ok) {
+        bool good = cudaEventCreateWithFlags(&p.fork, cudaEventDisableTiming) == cudaSuccess;
+        for (int k = 0; good && k < 2; ++k)
+            good = cudaStreamCreateWithFlags(&p.side[k], cudaStreamNonBlocking) == cudaSuccess &&
+                   cudaEventCreateWithFlags(&p.join[k], cudaEventDisableTiming) == cudaSuccess;
+        p.ok = good;
+    }
+    return p;
+}
+
+uint64_t wht_chunk(unsigned N) {
+    static const long env = [] {
+        const char* e = std::getenv("PD_WHT_CHUNK");
+        return e ? std::atol(e) : 0L;
+    }();
+    if (env > 0) return static_cast<uint64_t>(env);
+    const uint64_t s = (32ull << 20) / (sizeof(double2) << N);  // ~32 MiB of D' per chunk
+    return s < 32 ? 32 : s;
+}
+}  // namespace
+
+static cudaError_t wht_two_pass(const double2* G, unsigned N, uint64_t x0, uint64_t x_count,
+                                double2* dprime, const OutMap& map, bool l2_resident,
+                                cudaStream_t stream) {
     static std::atomic<uint64_t> attr_set{0};
     int dev = 0;
     cudaGetDevice(&dev);
     if (!(attr_set.load() >> dev & 1)) {
-        cudaError_t e = cudaFuncSetAttribute(wht_gather_lo_kernel,
+        cudaError_t e = cudaFuncSetAttribute(wht_gather_lo_kernel<true>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, kP1Smem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(wht_gather_lo_kernel<false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kP1Smem);
         if (e != cudaSuccess) return e;
         attr_set.fetch_or(1ull << dev);
     }
     const uint64_t grid1 = (x_count >> 5) << (N - kLoBits);
-    wht_gather_lo_kernel<<<static_cast<unsigned>(grid1), kWhtThreads, kP1Smem, stream>>>(G, N, x0, scratch);
+    auto k1 = l2_resident ? wht_gather_lo_kernel<true> : wht_gather_lo_kernel<false>;
+    k1<<<static_cast<unsigned>(grid1), kWhtThreads, kP1Smem, stream>>>(G, N, x0, dprime);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    if (launch_pass2(scratch, N, x0, x_count, map, stream) == cudaSuccess) {
+    if (launch_pass2(dprime, N, x0, x_count, map, l2_resident, stream) == cudaSuccess) {
         g_launches.fetch_add(1, std::memory_order_relaxed);
         return cudaGetLastError();
     }
@@ -413,7 +468,7 @@ cudaError_t launch_wht_from_matrix(const double2* G, unsigned N, uint64_t x0, ui
         auto k = wht_hi_out_kernel<HBV, XL>;                                                  \
         e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kP1Smem);    \
         if (e == cudaSuccess)                                                                 \
-            k<<<grid2, kWhtThreads, smem, stream>>>(scratch, N, x0, map, scale);             \
+            k<<<grid2, kWhtThreads, smem, stream>>>(dprime, N, x0, map, scale);              \
     } while (0)
     switch (hb * 4 + xpc_log) {
         case 1 * 4 + 2: PD_HI(1, 2); break;
@@ -431,6 +486,33 @@ cudaError_t launch_wht_from_matrix(const double2* G, unsigned N, uint64_t x0, ui
     if (e != cudaSuccess) return e;
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return cudaGetLastError();
+}
+
+cudaError_t launch_wht_from_matrix(const double2* G, unsigned N, uint64_t x0, uint64_t x_count,
+                                   double2* scratch, unsigned run_bits, double2* out, int layout,
+                                   cudaStream_t stream) {
+    const OutMap map = make_outmap(out, N, run_bits, layout);
+    const uint64_t S = wht_chunk(N);
+    const unsigned hb = N - kLoBits;
+    const bool reg_pass2 = hb >= 4 && hb <= 8;
+    if (!reg_pass2 || x_count < 2 * S || (S & 31) || x_count % S)
+        return wht_two_pass(G, N, x0, x_count, scratch, map, false, stream);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    WhtPipe& p = wht_pipe(dev);
+    if (!p.ok) return cudaErrorInitializationError;
+    const uint64_t dim = 1ull << N;
+    cudaError_t e = cudaEventRecord(p.fork, stream);
+    for (int k = 0; e == cudaSuccess && k < 2; ++k) e = cudaStreamWaitEvent(p.side[k], p.fork, 0);
+    for (uint64_t c = 0; e == cudaSuccess && c < x_count / S; ++c) {
+        const int k = static_cast<int>(c & 1);  // slot k of D' belongs to stream k
+        e = wht_two_pass(G, N, x0 + c * S, S, scratch + k * S * dim, map, true, p.side[k]);
+    }
+    for (int k = 0; e == cudaSuccess && k < 2; ++k) {
+        e = cudaEventRecord(p.join[k], p.side[k]);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, p.join[k], 0);
+    }
+    return e;
 }
 
 cudaError_t launch_wht_inplace(double2* rows, unsigned N, uint64_t x_count, cudaStream_t stream) {
