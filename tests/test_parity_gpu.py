@@ -272,3 +272,45 @@ def test_native_kernels_launched(pd, cuda):
     before = pd.launch_count()
     pd.decompose(np.eye(64, dtype=complex))
     assert pd.launch_count() >= before + 2  # K1 + K2
+
+
+def test_n15_maximum_single_gpu_size(pd, cuda):
+    """The largest full decomposition that fits one B200 with the scratch layout of
+    pd_decompose_device (G, D and the coefficients: 3 x 16 GiB): N=15, 1,073,741,824
+    coefficients. The Gray path (K1+K2) must equal the reference-order walk (K3, pinned to the
+    oracle at N <= 14) on 65,536 seeded strings bit for bit; Parseval over the whole array;
+    the WHT path within the tolerance."""
+    import torch
+    nq = 15
+    free, _ = torch.cuda.mem_get_info()
+    if free < 70 * 2**30:
+        pytest.skip("needs ~64 GiB of free device memory")
+    g = torch.empty((2**nq, 2**nq), dtype=torch.complex128, device=cuda)
+    pd.device.random_matrix(nq, 1515, g.data_ptr(), 0)
+    out = torch.empty(4**nq, dtype=torch.complex128, device=cuda)
+    scratch = torch.empty(4**nq, dtype=torch.complex128, device=cuda)
+    pd.device.decompose(nq, g.data_ptr(), out.data_ptr(), scratch.data_ptr(), "gray", 0)
+    ns = torch.from_numpy(np.sort(np.random.default_rng(15).choice(4**nq, 65536, replace=False))
+                          .astype(np.int64)).to(cuda)
+    walk = torch.empty(65536, dtype=torch.complex128, device=cuda)
+    pd.device.coeff_batch(nq, g.data_ptr(), ns.data_ptr(), 65536, False, walk.data_ptr(), 0)
+    torch.cuda.synchronize()
+    assert same_values(out[ns].cpu().numpy(), walk.cpu().numpy())
+    fro = float(torch.sum(torch.abs(g) ** 2))
+    par = float(2**nq * torch.sum(torch.abs(out) ** 2))
+    assert abs(fro - par) <= 1e-10 * fro
+    del walk
+    out2 = torch.empty_like(out)
+    pd.device.decompose(nq, g.data_ptr(), out2.data_ptr(), scratch.data_ptr(), "wht", 0)
+    torch.cuda.synchronize()
+    err = float(torch.max(torch.abs(out2 - out)) / torch.max(torch.abs(out)))
+    assert err <= TOL
+
+
+def test_empty_and_single_string_batches(pd, cuda, port):
+    rng = np.random.default_rng(3)
+    g = normal_matrix(rng, 4)
+    assert pd.coefficients(g, np.zeros(0, dtype=np.uint64)).shape == (0,)
+    want = port.decompose(g)
+    for n in (0, 1, 4**4 - 1):
+        assert same_values(pd.coefficients(g, np.array([n], dtype=np.uint64)), want[[n]])
