@@ -41,6 +41,9 @@ def parse_args():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--qubits", type=int, default=14)
     ap.add_argument("--path", choices=["gray", "wht"], default="gray")
+    ap.add_argument("--mode", choices=["nccl", "peer"], default="nccl",
+                    help="N>1 data path: NCCL broadcast + gather (north star) or CUDA-IPC peer "
+                         "memory (K1 reads rank 0's G, K2 stores into rank 0's output)")
     ap.add_argument("--sample-masks", type=int, default=64,
                     help="X-masks in the CPU sample (>= 8); 64 = 1,048,576 coefficients, ~10 s on 16 threads")
     ap.add_argument("--no-e2e", action="store_true")
@@ -49,7 +52,7 @@ def parse_args():
     return ap.parse_args()
 
 
-def workload_config(nq: int, world: int, path: str) -> dict:
+def workload_config(nq: int, world: int, path: str, mode: str = "nccl") -> dict:
     return {
         "workload": f"full decomposition N={nq} (BASELINE configs[4])" if nq == 14
         else f"full decomposition N={nq}",
@@ -58,7 +61,10 @@ def workload_config(nq: int, world: int, path: str) -> dict:
         "matrix": f"random_matrix({nq}, matrix_seed({ACCEPT_SEED},{nq},0)): uniform[-1,1) complex128, "
                   f"{16 * 4**nq / 2**30:g} GiB (reference generator, bit-exact on device)",
         "path": "gray-code K1+K2" if path == "gray" else "walsh-hadamard K1+K4",
-        "parallelism": f"xmask-shard x{world}" + (" (NCCL broadcast G + grouped send/recv gather)" if world > 1 else ""),
+        "parallelism": f"xmask-shard x{world}" + ((" (NCCL broadcast G + grouped send/recv gather)"
+                                                    if mode == "nccl" else
+                                                    " (CUDA-IPC peer memory: K1 reads rank 0's G, K2 stores into rank 0's output)")
+                                                   if world > 1 else ""),
         "l2": "inputs (4 GiB G, 4 GiB diagonals) exceed the 126 MB L2; no flush needed" if nq >= 12
         else "inputs smaller than L2",
     }
@@ -195,6 +201,10 @@ def run_reference_arm(args) -> None:
 
 # ---------------------------------------------------------------- our arm
 
+def sd_ptr(buf) -> int:
+    return buf.data_ptr() if hasattr(buf, "data_ptr") else int(buf)
+
+
 def run_ours(args) -> None:
     import numpy as np
     import torch
@@ -237,43 +247,51 @@ def run_ours(args) -> None:
         pd.device.random_matrix(nq, pd_seed, G.data_ptr(), sptr)
     diag = torch.empty(plan.x_count * dim, dtype=torch.complex128, device=dev)
     out = torch.empty(4**nq, dtype=torch.complex128, device=dev) if rank == 0 else None
-    local = None if rank == 0 else torch.empty(plan.run_len << plan.run_bits,
-                                               dtype=torch.complex128, device=dev)
-    # rank 0 writes its runs in place in the reference-ordered array; the others pack theirs
-    dst, layout = (out, "global") if rank == 0 else (local, "runs")
-    runs = [] if rank == 0 else \
-        [local[r * plan.run_len:(r + 1) * plan.run_len] for r in range(1 << plan.run_bits)]
+    peer = args.mode == "peer" and world > 1
+    local = None if rank == 0 or peer else torch.empty(plan.run_len << plan.run_bits,
+                                                       dtype=torch.complex128, device=dev)
+    from paper_2401_16378_b200.sharding import ShardedDecomposer
+    # the sharding layer's collectives (NCCL gather / peer mapping); K1 and K2 are launched here
+    # so that they can be timed apart
+    sd = ShardedDecomposer(nq, dev, mode=args.mode, path=args.path, buffers=False)
+    if peer:
+        # rank 0's G and output mapped into every rank once (CUDA IPC), outside the timed region
+        g_src, dst = sd.peer_buffers(G, out)
+        layout = "global"
+        torch.cuda.synchronize()
+        barrier()
+    else:
+        # rank 0 writes its runs in place in the reference-ordered array; the others pack theirs
+        g_src = G
+        dst, layout = (out, "global") if rank == 0 else (local, "runs")
+        sd.local = local
 
     def gather():
         if world == 1:
             return
-        ops = []
-        if rank == 0:
-            for src in range(1, world):
-                for o in plan.offsets(src):
-                    ops.append(dist.P2POp(dist.irecv, out[o:o + plan.run_len], src))
-        else:
-            for r in runs:
-                ops.append(dist.P2POp(dist.isend, r, 0))
-        for req in dist.batch_isend_irecv(ops):
-            req.wait()
+        if peer:  # the peers' K2 stores landed in rank 0's output; order them before its reads
+            torch.cuda.synchronize()
+            barrier()
+            return
+        sd.gather(out)
 
     def step(path, ev=None):
-        if world > 1:
+        if world > 1 and not peer:
             dist.broadcast(G, src=0)
         if ev is not None:
             ev[0].record(stream)
+        gp, dp = sd_ptr(g_src), sd_ptr(dst)
         if path == "gray":  # K1 and K2 timed separately
-            pd.device.diag_gather(nq, G.data_ptr(), plan.x0, plan.x_count, diag.data_ptr(), sptr)
+            pd.device.diag_gather(nq, gp, plan.x0, plan.x_count, diag.data_ptr(), sptr)
             if ev is not None:
                 ev[1].record(stream)
             pd.device.xmask_coeffs(nq, diag.data_ptr(), plan.x0, plan.x_count, plan.run_bits,
-                                   dst.data_ptr(), layout, path, sptr)
+                                   dp, layout, path, sptr)
         else:  # fused two-pass WHT straight from G
             if ev is not None:
                 ev[1].record(stream)
-            pd.device.shard_coeffs(nq, G.data_ptr(), plan.x0, plan.x_count, plan.run_bits,
-                                   dst.data_ptr(), layout, diag.data_ptr(), path, sptr)
+            pd.device.shard_coeffs(nq, gp, plan.x0, plan.x_count, plan.run_bits,
+                                   dp, layout, diag.data_ptr(), path, sptr)
         if ev is not None:
             ev[2].record(stream)
         gather()
@@ -348,7 +366,7 @@ def run_ours(args) -> None:
         "ms_per_step": per_step_ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": workload_config(nq, world, args.path),
+        "config": workload_config(nq, world, args.path, args.mode),
         "roofline": roofline,
         "gpu_launches": launches,
         "clocks": clocks,
@@ -466,7 +484,7 @@ def run_e2e(args, pd, plan, G, out, dev, stream, barrier, max_over_ranks, world,
                 "d2h_bytes_per_step": nbytes, "ms_per_step": per * 1e3,
                 "api": "paper_2401_16378_b200.decompose(pinned numpy, out=pinned numpy)"}
     from paper_2401_16378_b200.sharding import ShardedDecomposer
-    sd = ShardedDecomposer(nq, dev, path=args.path)
+    sd = ShardedDecomposer(nq, dev, path=args.path, mode=args.mode)
     gh_t = oh_t = None
     if rank == 0:
         gh_t = torch.empty(G.shape, dtype=torch.complex128, pin_memory=True)

@@ -176,6 +176,28 @@ PD_EXPORT int pd_first_nonfinite_device(const double* g, uint64_t count, uint64_
 PD_EXPORT int pd_host_alloc(size_t bytes, void** out);
 PD_EXPORT int pd_host_free(void* p);
 
+/* ---------------- peer memory (multi-GPU sharding over NVLink) ---------------- */
+
+/* A device buffer exported to the other processes of one box: the CUDA IPC handle of the
+ * allocation that contains it plus the buffer's offset inside that allocation (so buffers
+ * sub-allocated by a caching allocator can be shared). Plain bytes: send it through any
+ * host channel (the sharding layer uses torch.distributed object collectives). */
+typedef struct pd_ipc_handle {
+    unsigned char bytes[64];
+    uint64_t offset;
+} pd_ipc_handle;
+
+/* Export the allocation containing dev_ptr. */
+PD_EXPORT int pd_ipc_export(const void* dev_ptr, pd_ipc_handle* out);
+/* Map a peer's exported buffer into this process on the current device (peer access over
+ * NVLink/NVSwitch when the owner is another GPU); *dev_ptr = mapped base + offset. The kernels
+ * take such pointers like local ones: K1 gathers diagonals straight from the owner's G and K2
+ * stores coefficients straight into the owner's output (pd_shard_coeffs_device with
+ * PD_LAYOUT_GLOBAL), which replaces the broadcast and the gather of the NCCL sharding mode. */
+PD_EXPORT int pd_ipc_open(const pd_ipc_handle* handle, void** dev_ptr);
+/* Unmap a pointer returned by pd_ipc_open. */
+PD_EXPORT int pd_ipc_close(void* dev_ptr);
+
 /* ---------------- measurement helpers ---------------- */
 
 /* Number of kernels this library has launched in this process (all threads). */

@@ -12,6 +12,7 @@
 #include <pybind11/stl.h>
 
 #include <cstdint>
+#include <cstring>
 #include <string>
 #include <vector>
 
@@ -265,6 +266,23 @@ PYBIND11_MODULE(_paulidecomp, m) {
           py::arg("out"), py::arg("layout") = "global", py::arg("scratch") = 0,
           py::arg("path") = "gray", py::arg("stream") = 0,
           "All coefficients of an X-mask range straight from G (one shard's work).");
+    d.def("ipc_export", [](std::uintptr_t ptr) {
+        pd_ipc_handle h{};
+        check(pd_ipc_export(P<const void>(ptr), &h));
+        return py::make_tuple(py::bytes(reinterpret_cast<const char*>(h.bytes), sizeof(h.bytes)),
+                              h.offset);
+    }, py::arg("ptr"), "CUDA IPC export of the allocation holding ptr: (handle bytes, offset).");
+    d.def("ipc_open", [](const py::bytes& handle, std::uint64_t offset) {
+        pd_ipc_handle h{};
+        const std::string b = handle;
+        if (b.size() != sizeof(h.bytes)) throw std::invalid_argument("IPC handle must be 64 bytes");
+        std::memcpy(h.bytes, b.data(), sizeof(h.bytes));
+        h.offset = offset;
+        void* p = nullptr;
+        check(pd_ipc_open(&h, &p));
+        return reinterpret_cast<std::uintptr_t>(p);
+    }, py::arg("handle"), py::arg("offset"), "Map a peer's exported buffer; returns a device pointer.");
+    d.def("ipc_close", [](std::uintptr_t ptr) { check(pd_ipc_close(P<void>(ptr))); }, py::arg("ptr"));
     d.def("coeff_batch", [](unsigned N, std::uintptr_t g, std::uintptr_t ns, std::uint64_t count,
                             bool slow, std::uintptr_t out, std::uintptr_t stream) {
         check(pd_coeff_batch_device(N, P<const double>(g), P<const std::uint64_t>(ns), count,

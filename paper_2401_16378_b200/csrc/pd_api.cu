@@ -14,6 +14,8 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "pd_api.h"
 #include "pd_kernels.h"
@@ -621,6 +623,74 @@ int pd_oracle_coeff(pd_ctx* ctx, unsigned N, const double* g, uint64_t n, double
     if (e != cudaSuccess) return cuda_fail(e, "kron_trace launch");
     PD_CUDA(cudaMemcpyAsync(out, ctx->out, sizeof(double2), cudaMemcpyDeviceToHost, ctx->stream));
     PD_CUDA(cudaStreamSynchronize(ctx->stream));
+    return PD_OK;
+}
+
+namespace {
+typedef int (*MemGetAddressRange)(unsigned long long*, size_t*, unsigned long long);
+
+int allocation_base(const void* p, uintptr_t* base) {
+    static MemGetAddressRange fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return reinterpret_cast<MemGetAddressRange>(f);
+    }();
+    if (!fn) return fail(PD_ECUDA, "cuMemGetAddressRange unavailable");
+    unsigned long long b = 0;
+    size_t sz = 0;
+    if (fn(&b, &sz, reinterpret_cast<unsigned long long>(p)) != 0)
+        return fail(PD_EINVAL, "pointer %p is not device memory", p);
+    *base = static_cast<uintptr_t>(b);
+    return PD_OK;
+}
+
+std::mutex g_ipc_mu;
+std::vector<std::pair<void*, void*>> g_ipc_open;  // (returned pointer, mapped base)
+}  // namespace
+
+int pd_ipc_export(const void* dev_ptr, pd_ipc_handle* out) {
+    if (int rc = check_device()) return rc;
+    if (!dev_ptr || !out) return fail(PD_EINVAL, "null pointer");
+    uintptr_t base = 0;
+    if (int rc = allocation_base(dev_ptr, &base)) return rc;
+    cudaIpcMemHandle_t h;
+    PD_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+    static_assert(sizeof(h) <= sizeof(out->bytes), "IPC handle size");
+    std::memset(out->bytes, 0, sizeof(out->bytes));
+    std::memcpy(out->bytes, &h, sizeof(h));
+    out->offset = reinterpret_cast<uintptr_t>(dev_ptr) - base;
+    return PD_OK;
+}
+
+int pd_ipc_open(const pd_ipc_handle* handle, void** dev_ptr) {
+    if (int rc = check_device()) return rc;
+    if (!handle || !dev_ptr) return fail(PD_EINVAL, "null pointer");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle->bytes, sizeof(h));
+    void* base = nullptr;
+    PD_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+    *dev_ptr = static_cast<char*>(base) + handle->offset;
+    std::lock_guard<std::mutex> lk(g_ipc_mu);
+    g_ipc_open.emplace_back(*dev_ptr, base);
+    return PD_OK;
+}
+
+int pd_ipc_close(void* dev_ptr) {
+    void* base = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(g_ipc_mu);
+        for (size_t i = 0; i < g_ipc_open.size(); ++i)
+            if (g_ipc_open[i].first == dev_ptr) {
+                base = g_ipc_open[i].second;
+                g_ipc_open.erase(g_ipc_open.begin() + static_cast<long>(i));
+                break;
+            }
+    }
+    if (!base) return fail(PD_EINVAL, "pointer %p was not opened by pd_ipc_open", dev_ptr);
+    PD_CUDA(cudaIpcCloseMemHandle(base));
     return PD_OK;
 }
 

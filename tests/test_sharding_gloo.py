@@ -1,6 +1,8 @@
 """The multi-GPU sharding layer's host logic over real torch.distributed collectives
 (gloo, world sizes 2 and 4, CPU processes): X-mask partition, broadcast of G, run
-addressing and the grouped send/recv gather into rank 0's reference-ordered array.
+addressing and the grouped send/recv gather into rank 0's reference-ordered array (NCCL
+mode), and the handle publication, mapping cache and barrier ordering of the peer mode, with
+shared file mappings standing in for CUDA IPC.
 
 The device compute is replaced by a CPU stand-in built on the oracle (tests only), so the
 assembled output must equal the oracle's full decomposition value for value."""
@@ -22,12 +24,12 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-def _oracle_compute(G, x0, x_count, run_bits, dst, layout, diag):
+def _oracle_compute(N, G, x0, x_count, run_bits, dst, layout, diag):
     import sys
     sys.path.insert(0, ROOT)
     from oracle import oracle as O
-    g = G.numpy()
-    nq = g.shape[0].bit_length() - 1
+    nq = N
+    g = G.reshape(2**nq, 2**nq).numpy()
     low = 2 * (nq - run_bits)
     z = np.arange(2**nq, dtype=np.uint64)
     for x in range(x0, x0 + x_count):
@@ -42,7 +44,36 @@ def _oracle_compute(G, x0, x_count, run_bits, dst, layout, diag):
         dst[torch.from_numpy((rsel << low) | local)] = torch.from_numpy(vals)
 
 
-def _worker(rank, world, port, nq, result_path):
+class _FileMapper:
+    """CPU stand-in for CUDA IPC: rank 0's buffers live in shared file mappings, a handle is
+    (path, element count), and opening maps the same file (MAP_SHARED)."""
+
+    def __init__(self, tmpdir):
+        self.tmpdir = tmpdir
+        self.paths = {}
+
+    def alloc(self, name, shape):
+        path = os.path.join(self.tmpdir, name)
+        n = int(np.prod(shape))
+        t = torch.from_file(path, shared=True, size=n, dtype=torch.complex128).view(*shape)
+        self.paths[t.data_ptr()] = (path, n)
+        return t
+
+    def export(self, buf):
+        return self.paths[buf.data_ptr()]
+
+    def open(self, handle):
+        path, n = handle
+        return torch.from_file(path, shared=True, size=n, dtype=torch.complex128)
+
+    def close(self, mapped):
+        pass
+
+    def fence(self):
+        pass
+
+
+def _worker(rank, world, port, nq, result_path, mode="nccl"):
     import sys
     sys.path.insert(0, ROOT)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -50,26 +81,36 @@ def _worker(rank, world, port, nq, result_path):
     from paper_2401_16378_b200.sharding import ShardedDecomposer
     from oracle import oracle as O
     dim = 2**nq
+    mapper = _FileMapper(os.path.dirname(result_path)) if mode == "peer" else None
     if rank == 0:
-        G = torch.from_numpy(O.port().random_matrix(nq, 4242))
-        out = torch.zeros(4**nq, dtype=torch.complex128)
+        g0 = torch.from_numpy(O.port().random_matrix(nq, 4242))
+        if mapper:
+            G = mapper.alloc("G.bin", (dim, dim))
+            G.copy_(g0)
+            out = mapper.alloc("out.bin", (4**nq,))
+            out.zero_()
+        else:
+            G, out = g0, torch.zeros(4**nq, dtype=torch.complex128)
     else:
-        G = torch.zeros((dim, dim), dtype=torch.complex128)  # filled by the broadcast
+        G = torch.zeros((dim, dim), dtype=torch.complex128)  # filled by the broadcast (nccl mode)
         out = None
-    sd = ShardedDecomposer(nq, torch.device("cpu"), compute=_oracle_compute)
+    sd = ShardedDecomposer(nq, torch.device("cpu"), compute=_oracle_compute, mode=mode,
+                           mapper=mapper)
     assert sd.plan.x_count == dim // world and sd.plan.x0 == rank * dim // world
-    sd(G, out)
+    for _ in range(2):  # the second step reuses the cached peer mappings
+        sd(G, out)
     if rank == 0:
         np.save(result_path, out.numpy())
     dist.barrier()
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("mode", ["nccl", "peer"])
 @pytest.mark.parametrize("world", [2, 4])
-def test_sharded_gather_matches_oracle(tmp_path, world):
+def test_sharded_gather_matches_oracle(tmp_path, world, mode):
     nq = 5
     result = str(tmp_path / "out.npy")
-    mp.start_processes(_worker, args=(world, _free_port(), nq, result), nprocs=world,
+    mp.start_processes(_worker, args=(world, _free_port(), nq, result, mode), nprocs=world,
                        join=True, start_method="spawn")
     got = np.load(result)
     import sys
