@@ -488,6 +488,8 @@ static cudaError_t launch_walk_t(const double2* G, unsigned N, const uint64_t* n
 cudaError_t launch_walk(const double2* G, unsigned N, const uint64_t* ns, uint64_t count, bool slow,
                         double2* out, cudaStream_t stream) {
     if (count == 0) return cudaSuccess;
+    if (!slow && ns != nullptr && strings_grouped_ok(N, count))
+        return launch_strings_grouped(G, N, ns, count, out, stream);
     return slow ? launch_walk_t<true>(G, N, ns, count, out, stream)
                 : launch_walk_t<false>(G, N, ns, count, out, stream);
 }

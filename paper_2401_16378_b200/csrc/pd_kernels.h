@@ -33,6 +33,12 @@ cudaError_t launch_gray_xmask(const double2* diag, unsigned N, uint64_t x0, uint
                               unsigned run_bits, double2* out, int layout, cudaStream_t stream);
 uint64_t gray_xmask_grid(unsigned N, uint64_t x_count);
 
+// K3b: batched strings bucketed by X-mask, one CTA per X-mask over its staged diagonal
+// (bit-identical to K3); used by launch_walk when strings_grouped_ok
+bool strings_grouped_ok(unsigned N, uint64_t count);
+cudaError_t launch_strings_grouped(const double2* G, unsigned N, const uint64_t* ns,
+                                   uint64_t count, double2* out, cudaStream_t stream);
+
 // K4: fast Walsh-Hadamard path over the same diagonals (separately reported)
 cudaError_t launch_wht_xmask(const double2* diag, unsigned N, uint64_t x0, uint64_t x_count,
                              unsigned run_bits, double2* out, int layout, cudaStream_t stream);

@@ -314,3 +314,36 @@ def test_empty_and_single_string_batches(pd, cuda, port):
     want = port.decompose(g)
     for n in (0, 1, 4**4 - 1):
         assert same_values(pd.coefficients(g, np.array([n], dtype=np.uint64)), want[[n]])
+
+
+@pytest.mark.parametrize("nq,kind", [(5, "uniform"), (8, "one_xmask"), (9, "skewed"), (13, "uniform")])
+def test_grouped_strings_equal_reference_order_walk(pd, cuda, nq, kind):
+    """K3b (strings bucketed by X-mask, one CTA per bucket) must equal K3 (one thread per string
+    straight from G, selected here with slow=True) bit for bit, for bucket shapes the bucketing
+    can get wrong: a single X-mask holding every string, heavily skewed buckets, empty buckets,
+    duplicates, and the size limits N=5 and N=13."""
+    import torch
+    rng = np.random.default_rng(nq)
+    count = max(3 * 2**nq, 4096)
+    if kind == "uniform":
+        ns = rng.integers(0, 4**nq, count)
+    elif kind == "one_xmask":   # X-mask 0b1011 only: digits X/Y at bits 0,1,3, I/Z elsewhere
+        x = 0b1011
+        z = rng.integers(0, 2**nq, count)
+        ns = np.array([_n(x, int(zz), nq) for zz in z])
+    else:                       # 90 % of the strings in 4 X-masks
+        hot = rng.integers(0, 4**nq, 4)
+        ns = np.where(rng.random(count) < 0.9, hot[rng.integers(0, 4, count)], rng.integers(0, 4**nq, count))
+    ns = torch.from_numpy(ns.astype(np.int64)).to(cuda)
+    g = torch.from_numpy(normal_matrix(rng, nq)).to(cuda)
+    fast = torch.empty(count, dtype=torch.complex128, device=cuda)
+    ref = torch.empty_like(fast)
+    pd.device.coeff_batch(nq, g.data_ptr(), ns.data_ptr(), count, False, fast.data_ptr(), 0)
+    pd.device.coeff_batch(nq, g.data_ptr(), ns.data_ptr(), count, True, ref.data_ptr(), 0)
+    torch.cuda.synchronize()
+    assert same_values(fast.cpu().numpy(), ref.cpu().numpy())
+
+
+def _n(x, z, nq):
+    """tensor number of X-mask x and Z-mask z: digit t = 2 z_t + (x_t ^ z_t)"""
+    return sum((2 * ((z >> t) & 1) + (((x ^ z) >> t) & 1)) << (2 * t) for t in range(nq))
