@@ -125,6 +125,14 @@ PD_EXPORT uint64_t pd_scratch_bytes(unsigned num_qubits, uint64_t x_count, pd_pa
 PD_EXPORT int pd_decompose_device(unsigned num_qubits, const double* g, double* out, void* scratch,
                         pd_path path, void* stream);
 
+/* pd_decompose_device with a scratch buffer of any size >= pd_scratch_bytes(N, 32, path): the
+ * X-masks are processed in the largest power-of-two blocks whose diagonals fit scratch_bytes.
+ * This is what lets one 180 GB B200 hold N = 16 (G and the coefficients, 64 GiB each, plus a
+ * block of diagonals) where the one-shot form would need 192 GiB. */
+PD_EXPORT int pd_decompose_device_blocked(unsigned num_qubits, const double* g, double* out,
+                                          void* scratch, uint64_t scratch_bytes, pd_path path,
+                                          void* stream);
+
 /* K1: diag[(x - x0) * dim + i] = G[i ^ x][i] for x in [x0, x0 + x_count).
  * x_count is a power of two and x0 a multiple of it. */
 PD_EXPORT int pd_diag_gather_device(unsigned num_qubits, const double* g, uint64_t x0, uint64_t x_count,

@@ -235,6 +235,14 @@ PYBIND11_MODULE(_paulidecomp, m) {
                                   path_of(path), P<void>(stream)));
     }, py::arg("num_qubits"), py::arg("g"), py::arg("out"), py::arg("scratch"),
           py::arg("path") = "gray", py::arg("stream") = 0);
+    d.def("decompose_blocked", [](unsigned N, std::uintptr_t g, std::uintptr_t out,
+                                  std::uintptr_t scratch, std::uint64_t scratch_bytes,
+                                  const std::string& path, std::uintptr_t stream) {
+        check(pd_decompose_device_blocked(N, P<const double>(g), P<double>(out), P<void>(scratch),
+                                          scratch_bytes, path_of(path), P<void>(stream)));
+    }, py::arg("num_qubits"), py::arg("g"), py::arg("out"), py::arg("scratch"),
+          py::arg("scratch_bytes"), py::arg("path") = "gray", py::arg("stream") = 0,
+          "Full decomposition with a bounded scratch buffer (X-mask blocks).");
     d.def("diag_gather", [](unsigned N, std::uintptr_t g, std::uint64_t x0, std::uint64_t x_count,
                             std::uintptr_t diag, std::uintptr_t stream) {
         check(pd_diag_gather_device(N, P<const double>(g), x0, x_count, P<double>(diag),

@@ -320,6 +320,26 @@ int pd_decompose_device(unsigned N, const double* g, double* out, void* scratch,
                                   stream);
 }
 
+int pd_decompose_device_blocked(unsigned N, const double* g, double* out, void* scratch,
+                                uint64_t scratch_bytes, pd_path path, void* stream) {
+    if (int rc = check_qubits(N)) return rc;
+    if (int rc = check_device()) return rc;
+    if (path == PD_PATH_NAIVE) return pd_decompose_device(N, g, out, scratch, path, stream);
+    if (path != PD_PATH_GRAY && path != PD_PATH_WHT) return fail(PD_EINVAL, "unknown path");
+    if (!g || !out || !scratch) return fail(PD_EINVAL, "null buffer");
+    const uint64_t dim = 1ull << N;
+    uint64_t block = dim;
+    while (block > 1 && pd_scratch_bytes(N, block, path) > scratch_bytes) block >>= 1;
+    if (pd_scratch_bytes(N, block, path) > scratch_bytes || (block < 32 && block < dim))
+        return fail(PD_EINVAL, "scratch of %llu bytes holds fewer than 32 diagonals",
+                    static_cast<unsigned long long>(scratch_bytes));
+    for (uint64_t x0 = 0; x0 < dim; x0 += block)
+        if (int rc = pd_shard_coeffs_device(N, g, x0, block, 0, out, PD_LAYOUT_GLOBAL, scratch, path,
+                                            stream))
+            return rc;
+    return PD_OK;
+}
+
 int pd_coeff_batch_device(unsigned N, const double* g, const uint64_t* ns, uint64_t count, int slow,
                           double* out, void* stream) {
     if (int rc = check_qubits(N)) return rc;

@@ -347,3 +347,70 @@ def test_grouped_strings_equal_reference_order_walk(pd, cuda, nq, kind):
 def _n(x, z, nq):
     """tensor number of X-mask x and Z-mask z: digit t = 2 z_t + (x_t ^ z_t)"""
     return sum((2 * ((z >> t) & 1) + (((x ^ z) >> t) & 1)) << (2 * t) for t in range(nq))
+
+
+def test_blocked_scratch_matches_one_shot(pd, cuda):
+    import torch
+    nq = 11
+    g = torch.from_numpy(normal_matrix(np.random.default_rng(11), nq)).to(cuda)
+    full = torch.empty(4**nq, dtype=torch.complex128, device=cuda)
+    scratch = torch.empty(4**nq, dtype=torch.complex128, device=cuda)
+    for path in ("gray", "wht"):
+        pd.device.decompose(nq, g.data_ptr(), full.data_ptr(), scratch.data_ptr(), path, 0)
+        for blocks in (2, 8, 64):
+            out = torch.zeros_like(full)
+            pd.device.decompose_blocked(nq, g.data_ptr(), out.data_ptr(), scratch.data_ptr(),
+                                        16 * 4**nq // blocks, path, 0)
+            torch.cuda.synchronize()
+            assert torch.equal(out, full), (path, blocks)
+    with pytest.raises(ValueError):
+        pd.device.decompose_blocked(nq, g.data_ptr(), full.data_ptr(), scratch.data_ptr(),
+                                    16 * 2**nq * 8, "gray", 0)
+
+
+def test_n16_on_one_gpu_with_blocked_scratch(pd, cuda):
+    """N=16, 4,294,967,296 coefficients: G and the coefficients take 64 GiB each, so the
+    diagonals are processed in blocks of 4096 X-masks (16 GiB of scratch). Gray path checked
+    against the reference-order walk (K3) on 2,048 seeded strings bit for bit, Parseval over the
+    whole array, then the WHT path into the same buffer against the same sample and norm."""
+    import torch
+    nq = 16
+    free, _ = torch.cuda.mem_get_info()
+    if free < 150 * 2**30:
+        pytest.skip("needs ~145 GiB of free device memory")
+    g = torch.empty((2**nq, 2**nq), dtype=torch.complex128, device=cuda)
+    pd.device.random_matrix(nq, 1616, g.data_ptr(), 0)
+    out = torch.empty(4**nq, dtype=torch.complex128, device=cuda)
+    scratch = torch.empty(4096 * 2**nq, dtype=torch.complex128, device=cuda)
+    pd.device.decompose_blocked(nq, g.data_ptr(), out.data_ptr(), scratch.data_ptr(),
+                                scratch.numel() * 16, "gray", 0)
+    ns = torch.from_numpy(np.sort(np.random.default_rng(16).choice(4**nq, 2048, replace=False))
+                          .astype(np.int64)).to(cuda)
+    walk = torch.empty(2048, dtype=torch.complex128, device=cuda)
+    pd.device.coeff_batch(nq, g.data_ptr(), ns.data_ptr(), 2048, True, walk.data_ptr(), 0)
+    torch.cuda.synchronize()
+    gray_sample = out[ns].clone()
+    assert same_values(gray_sample.cpu().numpy(), walk.cpu().numpy())
+    fro = _sq_norm(g)
+    par = 2**nq * _sq_norm(out)
+    assert abs(fro - par) <= 1e-10 * fro
+    pd.device.decompose_blocked(nq, g.data_ptr(), out.data_ptr(), scratch.data_ptr(),
+                                scratch.numel() * 16, "wht", 0)
+    torch.cuda.synchronize()
+    err = float(torch.max(torch.abs(out[ns] - gray_sample)) / torch.max(torch.abs(gray_sample)))
+    assert err <= TOL
+    par2 = 2**nq * _sq_norm(out)
+    assert abs(fro - par2) <= 1e-10 * fro
+
+
+def _sq_norm(t):
+    """sum |t|^2 in 2^26-element slices (no full-size temporary)"""
+    v = t.reshape(-1)
+    step = 1 << 26
+    return float(sum(float(torch_sum_sq(v[i:i + step])) for i in range(0, v.numel(), step)))
+
+
+def torch_sum_sq(v):
+    import torch
+    r = torch.view_as_real(v)
+    return torch.sum(r * r)
