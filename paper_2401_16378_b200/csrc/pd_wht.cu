@@ -104,22 +104,25 @@ __global__ void __launch_bounds__(kWhtThreads)
 // ---------------------------------------------------------------------------------------
 // Fused two-pass WHT path (N >= 8): HBM traffic = read G + write D' + read D' + write out.
 //
-//   pass 1 (wht_gather_lo_kernel): CTA = 32 X-masks (one tile row block x_h) x 128 columns
+//   pass 1 (wht_gather_lo_reg_kernel): CTA = 32 X-masks (one tile row block x_h) x 128 columns
 //     (4 column blocks C). Tile (R = C ^ x_h, C) of G holds D_x[C*32 + c] at (r, c) with
-//     x = x_h*32 + (r ^ c) (the K1 transposition), so the 4 coalesced tile loads yield 32
-//     diagonal segments of 128; the low 7 index bits are butterflied in shared memory and
-//     the segments are written to D' (coalesced 2 KiB rows).
+//     x = x_h*32 + (r ^ c) (the K1 transposition), so the coalesced 512 B row loads yield 32
+//     diagonal segments of 128; index bits 5-6 are butterflied in registers, bits 0-4 in two
+//     shared-memory rounds, and the segments are written to D' (128 B lines).
 //   pass 2 (wht_hi_out_kernel): CTA = XPC X-masks x 8 adjacent low indices; loads 2^(N-7)
 //     128 B pieces per X-mask, butterflies the high N-7 bits, applies (-i)^{|x&z|} 2^-N and
 //     writes the coefficients: a warp covers (2 low x bits) x (3 low z bits), i.e. two
 //     contiguous 256 B runs of the reference-ordered array.
 //
-// Shared memory rows are padded by one element every 16 (pad(i) = i + i/16) so that both the
-// strided butterfly rounds and the XOR-permuted tile stores are bank-conflict free.
+// The generic pass 2 pads its shared-memory rows by one element every 16 (pad(i) = i + i/16)
+// so that the strided butterfly rounds are bank-conflict free.
 
 constexpr unsigned kLoBits = 7;  // index bits done in pass 1
 
 __device__ __forceinline__ unsigned pad16(unsigned i) { return i + (i >> 4); }
+
+// largest dynamic shared memory of the generic pass 2 (4096 padded elements)
+constexpr size_t kHiOutSmem = 32 * ((1u << kLoBits) + ((1u << kLoBits) >> 4)) * sizeof(double2);
 
 template <int RB>
 __device__ __forceinline__ void wht_round(double2* s, unsigned L, unsigned row_stride, unsigned rows,
@@ -149,46 +152,83 @@ __device__ __forceinline__ void wht_round(double2* s, unsigned L, unsigned row_s
     }
 }
 
-constexpr unsigned kP1Row = (1u << kLoBits) + ((1u << kLoBits) >> 4);  // 136 padded elements
-constexpr size_t kP1Smem = 32 * kP1Row * sizeof(double2);                // 69,632 B
+// Pass 1, register-first form: each thread loads the 4 column blocks of one
+// (row, column) position — the same X-mask x = r ^ c, index bits 5-6 — and butterflies them in
+// registers; bits 0-2 and 3-4 follow in two shared-memory rounds, the last storing from
+// registers. Rows padded to 33 elements (all access patterns conflict-free).
+constexpr unsigned kP1bRow = 33;
+constexpr size_t kP1bSmem = 128 * kP1bRow * sizeof(double2);               // 67,584 B
 
-template <bool KEEP>  // KEEP: D' stays in L2 for pass 2 (chunked pipeline); else streaming stores
+__device__ __forceinline__ void bfly(double2& a, double2& b) {
+    const double2 p = a, q = b;
+    a = make_double2(p.x + q.x, p.y + q.y);
+    b = make_double2(p.x - q.x, p.y - q.y);
+}
+
+template <bool KEEP>
 __global__ void __launch_bounds__(kWhtThreads, 2)
-    wht_gather_lo_kernel(const double2* __restrict__ G, unsigned N, uint64_t x0,
-                         double2* __restrict__ dprime) {
-    extern __shared__ __align__(16) double2 s1[];
+    wht_gather_lo_reg_kernel(const double2* __restrict__ G, unsigned N, uint64_t x0,
+                             double2* __restrict__ dprime) {
+    extern __shared__ __align__(16) double2 sb[];              // [x*4 + k][33]
     const uint64_t dim = 1ull << N;
-    const unsigned groups_log = N - kLoBits;                  // 128-column groups per row
+    const unsigned groups_log = N - kLoBits;
     const uint64_t grp = blockIdx.x & ((1u << groups_log) - 1);
-    const uint64_t xb = blockIdx.x >> groups_log;             // local block of 32 X-masks
+    const uint64_t xb = blockIdx.x >> groups_log;
     const uint64_t xh = (x0 >> 5) + xb;
-    constexpr int kIters = 4 * 1024 / kWhtThreads;            // 16 loads in flight per thread
-    double2 v[kIters];
+    const unsigned c = threadIdx.x & 31, w = threadIdx.x >> 5;
+    double2 v[4][4];
 #pragma unroll
-    for (int it = 0; it < kIters; ++it) {
-        const unsigned e = threadIdx.x + it * kWhtThreads;
-        const unsigned cb = e >> 10, r = (e >> 5) & 31, c = e & 31;
-        const uint64_t C = grp * 4 + cb, R = C ^ xh;
-        v[it] = __ldcs(&G[((R << 5) + r) * dim + (C << 5) + c]);
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int cb = 0; cb < 4; ++cb) {
+            const uint64_t C = grp * 4 + cb, R = C ^ xh;
+            v[j][cb] = __ldcs(&G[((R << 5) + w + 8 * j) * dim + (C << 5) + c]);
+        }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        bfly(v[j][0], v[j][1]);
+        bfly(v[j][2], v[j][3]);
+        bfly(v[j][0], v[j][2]);
+        bfly(v[j][1], v[j][3]);
+        const unsigned x5 = (w + 8 * j) ^ c;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) sb[(x5 * 4 + k) * kP1bRow + c] = v[j][k];
     }
+    __syncthreads();
 #pragma unroll
-    for (int it = 0; it < kIters; ++it) {
-        const unsigned e = threadIdx.x + it * kWhtThreads;
-        const unsigned cb = e >> 10, r = (e >> 5) & 31, c = e & 31;
-        s1[(r ^ c) * kP1Row + pad16(cb * 32 + c)] = v[it];
+    for (int q = 0; q < 2; ++q) {
+        const unsigned g = threadIdx.x + q * kWhtThreads, row = g & 127, chi = g >> 7;
+        double2* r = sb + row * kP1bRow + chi * 8;
+        double2 u[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) u[e] = r[e];
+#pragma unroll
+        for (int h = 1; h < 8; h <<= 1)
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+                if (!(e & h)) bfly(u[e], u[e + h]);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) r[e] = u[e];
     }
     __syncthreads();
-    wht_round<4>(s1, kLoBits, kP1Row, 32, 3);
-    __syncthreads();
-    wht_round<3>(s1, kLoBits, kP1Row, 32, 0);
-    __syncthreads();
 #pragma unroll
-    for (int it = 0; it < kIters; ++it) {
-        const unsigned e = threadIdx.x + it * kWhtThreads;
-        const unsigned row = e >> 7, il = e & 127;
-        double2* dst = &dprime[((xb << 5) + row) * dim + (grp << kLoBits) + il];
-        if (KEEP) *dst = s1[row * kP1Row + pad16(il)];
-        else __stcs(dst, s1[row * kP1Row + pad16(il)]);
+    for (int q = 0; q < 4; ++q) {
+        const unsigned g = threadIdx.x + q * kWhtThreads, clo = g & 7, row = g >> 3;
+        const double2* r = sb + row * kP1bRow + clo;
+        double2 u[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) u[h] = r[h * 8];
+        bfly(u[0], u[1]);
+        bfly(u[2], u[3]);
+        bfly(u[0], u[2]);
+        bfly(u[1], u[3]);
+        const unsigned x5 = row >> 2, k = row & 3;
+        double2* dst = dprime + ((xb << 5) + x5) * dim + (grp << kLoBits) + k * 32 + clo;
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            if (KEEP) dst[h * 8] = u[h];
+            else __stcs(dst + h * 8, u[h]);
+        }
     }
 }
 
@@ -437,17 +477,16 @@ static cudaError_t wht_two_pass(const double2* G, unsigned N, uint64_t x0, uint6
     int dev = 0;
     cudaGetDevice(&dev);
     if (!(attr_set.load() >> dev & 1)) {
-        cudaError_t e = cudaFuncSetAttribute(wht_gather_lo_kernel<true>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kP1Smem);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(wht_gather_lo_kernel<false>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kP1Smem);
+        cudaError_t e = cudaSuccess;
+        for (auto k : {wht_gather_lo_reg_kernel<true>, wht_gather_lo_reg_kernel<false>})
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kP1bSmem);
         if (e != cudaSuccess) return e;
         attr_set.fetch_or(1ull << dev);
     }
     const uint64_t grid1 = (x_count >> 5) << (N - kLoBits);
-    auto k1 = l2_resident ? wht_gather_lo_kernel<true> : wht_gather_lo_kernel<false>;
-    k1<<<static_cast<unsigned>(grid1), kWhtThreads, kP1Smem, stream>>>(G, N, x0, dprime);
+    auto k1 = l2_resident ? wht_gather_lo_reg_kernel<true> : wht_gather_lo_reg_kernel<false>;
+    k1<<<static_cast<unsigned>(grid1), kWhtThreads, kP1bSmem, stream>>>(G, N, x0, dprime);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -466,7 +505,7 @@ static cudaError_t wht_two_pass(const double2* G, unsigned N, uint64_t x0, uint6
 #define PD_HI(HBV, XL)                                                                        \
     do {                                                                                      \
         auto k = wht_hi_out_kernel<HBV, XL>;                                                  \
-        e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kP1Smem);    \
+        e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kHiOutSmem); \
         if (e == cudaSuccess)                                                                 \
             k<<<grid2, kWhtThreads, smem, stream>>>(dprime, N, x0, map, scale);              \
     } while (0)

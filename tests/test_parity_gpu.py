@@ -282,6 +282,7 @@ def test_n15_maximum_single_gpu_size(pd, cuda):
     the WHT path within the tolerance."""
     import torch
     nq = 15
+    torch.cuda.empty_cache()  # earlier tests' cached blocks
     free, _ = torch.cuda.mem_get_info()
     if free < 70 * 2**30:
         pytest.skip("needs ~64 GiB of free device memory")
@@ -375,6 +376,7 @@ def test_n16_on_one_gpu_with_blocked_scratch(pd, cuda):
     whole array, then the WHT path into the same buffer against the same sample and norm."""
     import torch
     nq = 16
+    torch.cuda.empty_cache()  # earlier tests' cached blocks
     free, _ = torch.cuda.mem_get_info()
     if free < 150 * 2**30:
         pytest.skip("needs ~145 GiB of free device memory")
