@@ -416,3 +416,25 @@ def torch_sum_sq(v):
     import torch
     r = torch.view_as_real(v)
     return torch.sum(r * r)
+
+
+def test_array_like_inputs_are_coerced_like_the_reference_binding(pd, cuda, port):
+    """module.cpp:21 of the reference takes any array-like through pybind's forcecast to a
+    C-contiguous complex128 array: lists, real or integer arrays, transposed / Fortran-ordered
+    and strided views must all decompose exactly like their complex128 C-contiguous copy."""
+    rng = np.random.default_rng(21)
+    g = normal_matrix(rng, 4)
+    want = port.decompose(np.ascontiguousarray(g))
+    assert same_values(pd.decompose(g.tolist()), want)
+    gt = np.ascontiguousarray(g.T)
+    assert same_values(pd.decompose(g.T.T), want)
+    assert same_values(pd.decompose(np.asfortranarray(g)), want)
+    assert same_values(pd.decompose(gt.T), want)                      # non-contiguous view
+    big = np.zeros((32, 32), dtype=complex)
+    big[::2, ::2] = g
+    assert same_values(pd.decompose(big[::2, ::2]), want)             # strided view
+    r = rng.standard_normal((16, 16))
+    assert same_values(pd.decompose(r), port.decompose(r.astype(complex)))
+    i = rng.integers(-3, 4, (8, 8))
+    assert same_values(pd.decompose(i), port.decompose(i.astype(complex)))
+    assert same_values(pd.coefficients(g.tolist(), [0, 5, 255]), want[[0, 5, 255]])
