@@ -1,0 +1,75 @@
+#!/usr/bin/env python
+"""Write profiles/r01_ncu.md from the committed evidence of one round:
+
+    python profiles/summarize_round.py
+
+inputs (all under profiles/): r01_bench_final.json (bench.py default line), r01_launches_N14_bench.csv
+(ncu launch list of the bench command), r01_prof_gray_N14.ncu-rep and r01_prof_wht_N14_chunked.ncu-rep
+(ncu --set full captures), ncu_traffic.json (range-replay DRAM bytes of whole decompositions)."""
+import json
+import os
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+from ncu_summary import launches, report  # noqa: E402
+
+CMDS = """```
+python bench.py --steps 3 --warmup 3 --no-cpu-baseline && \\
+ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline
+C1="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-extras"
+ncu --set full --clock-control none --import-source on -k regex:"gray_xmask|diag_gather" -c 2 -o prof_gray $C1
+C2="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-extras --path wht"
+ncu --set full --clock-control none --import-source on -k regex:"wht" -s 300 -c 2 -o prof_wht $C2
+ncu --replay-mode range --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,lts__t_sector_hit_rate.pct \\
+    python gpurun_exp/wht_range.py <lib>        (PD_PATH=1 WHT, PD_PATH=0 Gray: one pd_decompose_device call)
+```"""
+
+
+def main():
+    b = json.load(open(os.path.join(HERE, "r01_bench_final.json")))
+    r, w, sc, cb = b["roofline"], b["wht_path"], b["side_configs"], b["cpu_baseline"]
+    rows = [
+        ("N=14 Gray path (K1+K2), device-resident",
+         f"{b['ms_per_step']:.2f} ms/step = {b['value'] / 1e6:.1f} M coeff/s"),
+        ("K2 roofline", f"{r['achieved']:.2f} of {r['peak']:.2f} TFLOP/s nominal FP64-add = **{100 * r['frac']:.1f} %** "
+                        f"({100 * r['frac_of_probe']:.1f} % of the live DADD probe, {r['probe_tflops']:.2f})"),
+        ("K1 diagonal gather", f"{r['k1_gather_ms']:.3f} ms = {r['k1_gather_gbs']:.0f} GB/s "
+                               f"({100 * r['k1_gather_gbs'] / 6542.7:.1f} % of measured 6542.7)"),
+        ("e2e `decompose(pinned host G, out=pinned host)`",
+         f"{b['e2e']['ms_per_step']:.1f} ms = {b['e2e']['value'] / 1e6:.1f} M coeff/s (8 GiB of H2D+D2H inside)"),
+        ("WHT path (chunked L2-resident two-pass)",
+         f"{w['ms_per_step']:.3f} ms = {w['value'] / 1e9:.1f} G coeff/s; {w['roofline']['achieved']:.0f} GB/s "
+         f"algorithmic = {100 * w['roofline']['frac']:.1f} % of measured HBM"),
+        ("N=12 full (configs[3])", f"{sc['n12_full_gray']['ms_per_step']:.3f} ms, "
+                                   f"{100 * sc['n12_full_gray']['fp64_frac_incl_k1']:.1f} % of FP64 peak incl. K1"),
+        ("N=10 65,536 strings (configs[1])", f"{1e3 * sc['n10_strings']['ms_per_step']:.1f} us"),
+        ("CPU reference (oracle/_ref, coeff_fast)",
+         f"{cb['value']:.0f} coeff/s, {cb['cores']} threads, {cb['sample']}; GPU/CPU = {b['value'] / cb['value']:.0f}x"),
+        ("clocks during the timed region", f"{b['clocks']['sm_mhz']:.0f} / {b['clocks']['sm_max_mhz']:.0f} MHz, "
+                                           f"reasons {b['clocks']['reasons']}"),
+    ]
+    t = json.load(open(os.path.join(HERE, "ncu_traffic.json")))
+    out = ["# Round 1 ncu evidence (B200, N=14 full decomposition)", "",
+           "Commands (each run only after the same command exited 0 without ncu, "
+           "`gpurun_exp/round_evidence.sh`):", "", CMDS, "",
+           "## Headline (bench.py default, `r01_bench_final.json`)", "", "| quantity | value |", "|---|---|"]
+    out += [f"| {k} | {v} |" for k, v in rows]
+    out += ["", "## DRAM traffic of a whole decomposition (range replay)", "",
+            f"* Gray (K1 + K2): {t['N14_gray_range_read'] / 1e9:.2f} GB read + {t['N14_gray_range_write'] / 1e9:.2f} GB "
+            f"written (algorithmic: K1 8.59 GB + K2 8.59 GB).",
+            f"* WHT chunked: {t['N14_wht_range_read'] / 1e9:.2f} GB read + {t['N14_wht_range_write'] / 1e9:.2f} GB written "
+            f"(algorithmic 8.59 GB; the one-chunk design moved 17.1 GB). D' never leaves L2.", "",
+            "## Launch list of the default bench command (cold-cache, serialised — compare shares)", "",
+            launches(os.path.join(HERE, "r01_launches_N14_bench.csv")), "",
+            "(`gray_xmask_kernel<4,1,0>` is the segmented K2 of the pipelined host path inside the e2e "
+            "measurement; `<4,0,0>` the device-resident one; the WHT kernels run once per 128-X-mask chunk, "
+            "the strings kernels once per configs[1] batch.)", "",
+            "## Full-set captures", "",
+            report(os.path.join(HERE, "r01_prof_gray_N14.ncu-rep")), "",
+            report(os.path.join(HERE, "r01_prof_wht_N14_chunked.ncu-rep"))]
+    open(os.path.join(HERE, "r01_ncu.md"), "w").write("\n".join(out) + "\n")
+
+
+if __name__ == "__main__":
+    main()
