@@ -106,6 +106,10 @@ unsigned flipped_bit_index(std::uint64_t k);
 
 // all 4^N coefficients of the row-major matrix at g into out (4^N entries)
 void decompose_into(const Complex* g, unsigned num_qubits, Complex* out, Path path = Path::Gray);
+// the same over several GPUs of this host (pd_ctx_create_multi: X-masks split across the
+// devices, each uploading only the 1/P of G it needs); a device may be listed more than once
+void decompose_into(const Complex* g, unsigned num_qubits, Complex* out, Path path,
+                    const std::vector<int>& devices);
 PauliDecomposition decompose(const DenseMatrix& g, Path path = Path::Gray);
 
 // out[k] = c_{ns[k]}

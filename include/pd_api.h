@@ -74,6 +74,12 @@ PD_EXPORT int pd_api_version(void);
  * One host thread per context (the reference's calls are synchronous). */
 PD_EXPORT int pd_ctx_create(int device, pd_ctx** out);
 PD_EXPORT int pd_ctx_destroy(pd_ctx* ctx);
+/* Multi-device context over count = 2^p GPUs of one host (a device may be listed more than
+ * once). pd_decompose on it splits the X-masks across the devices: device g uploads only the
+ * 1/P of G its diagonals touch, computes its block and downloads its coefficient runs straight
+ * into `out`, with no device-to-device traffic; results are bit-identical to one device. The
+ * multi-device analogue of decompose_parallel's `threads` (decompose.cpp:95-131). */
+PD_EXPORT int pd_ctx_create_multi(const int* devices, int count, pd_ctx** out);
 /* the context's stream, as a cudaStream_t */
 PD_EXPORT void* pd_ctx_stream(pd_ctx* ctx);
 

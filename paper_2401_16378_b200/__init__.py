@@ -4,7 +4,7 @@ Drop-in for the reference package ``paulidecomp`` (proj/python/paulidecomp/__ini
 the same public names, argument meanings and exceptions, served by hand-written CUDA
 kernels through the C ABI in ``include/pd_api.h``:
 
-    decompose(matrix, threads=1, serial=False, path="gray", out=None)
+    decompose(matrix, threads=1, serial=False, path="gray", out=None, devices=None)
     coefficient(matrix, n | label, slow=False)
     oracle_coefficient(matrix, n | label)
     recompose(coefficients)

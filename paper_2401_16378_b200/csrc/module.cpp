@@ -41,7 +41,7 @@ Path parse_path(const std::string& s) {
 }
 
 py::array_t<Complex> py_decompose(const ComplexArray& g, unsigned threads, bool serial,
-                                  const std::string& path, py::object out) {
+                                  const std::string& path, py::object out, py::object devices) {
     const unsigned N = matrix_qubits(g);
     if (threads == 0) throw std::invalid_argument("thread count must be at least 1");
     (void)serial;  // the quaternary driver yields the same coefficients (decompose.cpp:133-152)
@@ -59,9 +59,12 @@ py::array_t<Complex> py_decompose(const ComplexArray& g, unsigned threads, bool 
     }
     const Complex* src = g.data();
     Complex* dst = result.mutable_data();
+    std::vector<int> devs;
+    if (!devices.is_none()) devs = devices.cast<std::vector<int>>();
     {
         py::gil_scoped_release nogil;
-        decompose_into(src, N, dst, p);
+        if (!devs.empty()) decompose_into(src, N, dst, p, devs);
+        else decompose_into(src, N, dst, p);
     }
     return result;
 }
@@ -146,7 +149,9 @@ PYBIND11_MODULE(_paulidecomp, m) {
 
     m.def("decompose", &py_decompose, py::arg("matrix"), py::arg("threads") = 1,
           py::arg("serial") = false, py::arg("path") = "gray", py::arg("out") = py::none(),
-          "All 4**N expansion coefficients of a 2**N x 2**N matrix, indexed by tensor number.");
+          py::arg("devices") = py::none(),
+          "All 4**N expansion coefficients of a 2**N x 2**N matrix, indexed by tensor number. "
+          "devices=[d0, d1, ...] (a power-of-two count) splits the X-masks over those GPUs.");
     m.def("recompose", &py_recompose, py::arg("coefficients"),
           "Rebuild the dense matrix from its full coefficient vector.");
     m.def("coefficient", &py_coefficient_index, py::arg("matrix"), py::arg("n"),

@@ -5,6 +5,7 @@
 
 #include <bit>
 #include <memory>
+#include <map>
 #include <mutex>
 #include <new>
 #include <string>
@@ -115,6 +116,30 @@ void decompose_into(const Complex* g, unsigned num_qubits, Complex* out, Path pa
     check_qubit_count(num_qubits);
     Lease l = lease();
     raise(pd_decompose(l.ctx, num_qubits, as_doubles(g), as_doubles(out),
+                       static_cast<pd_path>(static_cast<int>(path))));
+}
+
+void decompose_into(const Complex* g, unsigned num_qubits, Complex* out, Path path,
+                    const std::vector<int>& devices) {
+    check_qubit_count(num_qubits);
+    if (devices.empty()) {
+        decompose_into(g, num_qubits, out, path);
+        return;
+    }
+    // one multi-device context per device list, serialised like the single-device ones
+    static std::mutex mu;
+    static std::map<std::vector<int>, std::unique_ptr<Device>> contexts;
+    Device* d;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto& slot = contexts[devices];
+        if (!slot) slot = std::make_unique<Device>();
+        d = slot.get();
+    }
+    std::lock_guard<std::mutex> lk(d->mu);
+    if (!d->ctx)
+        raise(pd_ctx_create_multi(devices.data(), static_cast<int>(devices.size()), &d->ctx));
+    raise(pd_decompose(d->ctx, num_qubits, as_doubles(g), as_doubles(out),
                        static_cast<pd_path>(static_cast<int>(path))));
 }
 

@@ -123,6 +123,7 @@ struct pd_ctx {
     size_t scratch_bytes = 0;
     void* ns = nullptr;
     size_t ns_bytes = 0;
+    std::vector<pd_ctx*> subs;       // multi-device context: one sub-context per listed device
 
     int ensure(void** p, size_t* have, size_t need) {
         if (*have >= need) return PD_OK;
@@ -190,8 +191,29 @@ int pd_ctx_create(int device, pd_ctx** out) {
     return PD_OK;
 }
 
+int pd_ctx_create_multi(const int* devices, int count, pd_ctx** out) {
+    if (!out || !devices) return fail(PD_EINVAL, "null pointer");
+    *out = nullptr;
+    if (count < 1 || (count & (count - 1)) || count > 256)
+        return fail(PD_EINVAL, "device count must be a power of two in [1, 256]");
+    pd_ctx* parent = nullptr;
+    if (int rc = pd_ctx_create(devices[0], &parent)) return rc;
+    for (int k = 0; k < count; ++k) {
+        pd_ctx* sub = nullptr;
+        if (int rc = pd_ctx_create(devices[k], &sub)) {
+            pd_ctx_destroy(parent);
+            return rc;
+        }
+        parent->subs.push_back(sub);
+    }
+    *out = parent;
+    return PD_OK;
+}
+
 int pd_ctx_destroy(pd_ctx* ctx) {
     if (!ctx) return PD_OK;
+    for (pd_ctx* sub : ctx->subs) pd_ctx_destroy(sub);
+    ctx->subs.clear();
     cudaSetDevice(ctx->device);
     for (cudaStream_t s : {ctx->stream, ctx->stream2, ctx->d2h, ctx->h2d})
         if (s) cudaStreamSynchronize(s);
@@ -382,10 +404,15 @@ namespace {
 int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_path path);
 }
 
+namespace {
+int decompose_multi(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_path path);
+}
+
 int pd_decompose(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_path path) {
     if (int rc = check_qubits(N)) return rc;
     if (int rc = bind(ctx)) return rc;
     if (!g || !out) return fail(PD_EINVAL, "null buffer");
+    if (ctx->subs.size() > 1) return decompose_multi(ctx, N, g, out, path);
     return decompose_host(ctx, N, g, out, path);
 }
 
@@ -563,6 +590,56 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
     PD_CUDA(cudaStreamSynchronize(ctx->stream2));
     PD_CUDA(cudaStreamSynchronize(ctx->h2d));
     return PD_OK;
+}
+
+}  // namespace
+
+namespace {
+
+// Multi-device host path (pd_ctx_create_multi): device g of P = 2^p owns the X-masks whose top
+// p bits equal g. Its diagonals touch only the P tiles (row block t ^ g, column block t) of G,
+// so it uploads exactly those (1/P of G) straight from the host, runs K1+K2 (or the WHT) on
+// its block with the runs packed (PD_LAYOUT_RUNS), and downloads its 2^p runs straight to their
+// offsets of the host output: every transfer goes over the device's own host link and there is
+// no device-to-device traffic at all. The devices' work is issued asynchronously from this
+// thread and overlaps; results are bit-identical to one device.
+int decompose_multi(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_path path) {
+    const uint64_t P = ctx->subs.size();
+    const unsigned p = static_cast<unsigned>(__builtin_ctzll(P));
+    const uint64_t dim = 1ull << N;
+    if (P > dim) return fail(PD_EINVAL, "more devices (%llu) than X-masks (%llu)",
+                             static_cast<unsigned long long>(P), static_cast<unsigned long long>(dim));
+    if (path != PD_PATH_GRAY && path != PD_PATH_WHT)
+        return fail(PD_EINVAL, "multi-device decompositions run the GRAY or WHT path");
+    const uint64_t B = dim >> p;                       // tile edge = X-masks per device
+    const uint64_t run_len = 1ull << (2 * (N - p));
+    for (uint64_t d = 0; d < P; ++d) {
+        pd_ctx* s = ctx->subs[d];
+        if (int rc = bind(s)) return rc;
+        const size_t gbytes = elems(N) * sizeof(double2);
+        if (int rc = s->ensure(&s->g, &s->g_bytes, gbytes)) return rc;
+        if (int rc = s->ensure(&s->out, &s->out_bytes, (elems(N) >> p) * sizeof(double2))) return rc;
+        const uint64_t sb = pd_scratch_bytes(N, B < 32 ? 32 : B, path);
+        if (int rc = s->ensure(&s->scratch, &s->scratch_bytes, sb)) return rc;
+        double* gd = static_cast<double*>(s->g);
+        for (uint64_t t = 0; t < P; ++t) {
+            const uint64_t off = 2 * (((t ^ d) * B) * dim + t * B);  // tile (t ^ d, t), in doubles
+            PD_CUDA(cudaMemcpy2DAsync(gd + off, dim * sizeof(double2), g + off, dim * sizeof(double2),
+                                      B * sizeof(double2), B, cudaMemcpyHostToDevice, s->stream));
+        }
+        if (int rc = pd_shard_coeffs_device(N, gd, d * B, B, p, static_cast<double*>(s->out),
+                                            PD_LAYOUT_RUNS, s->scratch, path, s->stream))
+            return rc;
+        for (uint64_t r = 0; r < P; ++r)
+            PD_CUDA(cudaMemcpyAsync(out + 2 * pd_run_offset(N, p, d, r),
+                                    static_cast<double*>(s->out) + 2 * r * run_len,
+                                    run_len * sizeof(double2), cudaMemcpyDeviceToHost, s->stream));
+    }
+    for (pd_ctx* s : ctx->subs) {
+        if (int rc = bind(s)) return rc;
+        PD_CUDA(cudaStreamSynchronize(s->stream));
+    }
+    return bind(ctx);
 }
 
 }  // namespace

@@ -438,3 +438,16 @@ def test_array_like_inputs_are_coerced_like_the_reference_binding(pd, cuda, port
     i = rng.integers(-3, 4, (8, 8))
     assert same_values(pd.decompose(i), port.decompose(i.astype(complex)))
     assert same_values(pd.coefficients(g.tolist(), [0, 5, 255]), want[[0, 5, 255]])
+
+
+@pytest.mark.parametrize("devices", [[0, 0], [0, 0, 0, 0], [0] * 8])
+@pytest.mark.parametrize("nq,path", [(9, "gray"), (12, "gray"), (12, "wht")])
+def test_multi_device_context_matches_one_device(pd, cuda, devices, nq, path):
+    """pd_ctx_create_multi on a list that repeats device 0: every virtual device gets its own
+    streams and buffers (left uninitialised), uploads only the tiles (t ^ g, t) of G its
+    X-masks touch and downloads its runs to their offsets — a missing tile or a misplaced run
+    shows up as a mismatch. No kernel waits on another, so sharing one GPU is safe."""
+    g = normal_matrix(np.random.default_rng(nq), nq)
+    want = pd.decompose(g, path=path)
+    got = pd.decompose(g, path=path, devices=devices)
+    assert np.array_equal(got, want)
