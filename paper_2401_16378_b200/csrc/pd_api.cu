@@ -510,9 +510,9 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
         return PD_OK;
     }
     // Pipelined host path.
-    //  * Upload. Gray path with >= 2 walk chunks (N >= 12): G goes up in column segments in
-    //    the Gray order of the walk (columns [gray(s) W, gray(s) W + W) are exactly the
-    //    diagonal indices visited by walk segment s), each followed by K1 on those columns,
+    //  * Upload. Gray path with >= 2 walk chunks (N >= 12): G goes up in column segments that
+    //    follow the walk (chunks [1, 2), [2, 4), [4, 8) ... visit exactly the columns of the
+    //    same ranges times the chunk length), each followed by K1 on those columns,
     //    while K2 runs the previous walk segment; K2 segments chain through raw partial sums,
     //    so the result is bit-identical to one launch. Otherwise G goes up in one copy.
     //  * Download. The last K2 segment (or the whole WHT) runs in 16 X-mask blocks alternating
@@ -532,9 +532,18 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
     if (gray && segs >= 2) {
         if (int rc = ctx->ensure(&ctx->part, &ctx->part_bytes, bytes)) return rc;
         part = static_cast<double2*>(ctx->part);
-        const uint64_t W = dim / segs;
-        for (unsigned sg = 0; sg < segs; ++sg) {
-            const uint64_t col0 = (sg ^ (sg >> 1)) * W;  // Gray order of the walk segments
+        // walk segments [bnd[k], bnd[k+1]) in chunks, growing 1, 1, 2, 4, ... so that the first
+        // upload (the only one not hidden behind K2) is small; an aligned power-of-two run of
+        // chunks covers a contiguous column range (gray() permutes it onto itself)
+        unsigned bnd[pd_ctx::kSegs + 1];
+        unsigned nb = 0;
+        bnd[nb++] = 0;
+        for (unsigned c = 1; nb < segs && c < nch; c <<= 1) bnd[nb++] = c;
+        bnd[nb] = nch;
+        const unsigned nseg = nb;
+        const uint64_t C = dim / nch;  // columns per walk chunk
+        for (unsigned sg = 0; sg < nseg; ++sg) {
+            const uint64_t col0 = bnd[sg] * C, W = (bnd[sg + 1] - bnd[sg]) * C;
             PD_CUDA(cudaMemcpy2DAsync(gdev + 2 * col0, dim * sizeof(double2), g + 2 * col0,
                                       dim * sizeof(double2), W * sizeof(double2), dim,
                                       cudaMemcpyHostToDevice, ctx->h2d));
@@ -544,17 +553,16 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
             if (e != cudaSuccess) return cuda_fail(e, "diag_gather launch");
             PD_CUDA(cudaEventRecord(ctx->cols_ready[sg], ctx->h2d));
         }
-        const unsigned per = nch / segs;
-        for (unsigned sg = 0; sg + 1 < segs; ++sg) {
+        for (unsigned sg = 0; sg + 1 < nseg; ++sg) {
             PD_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->cols_ready[sg], 0));
             cudaError_t e = pdb::launch_gray_segment(reinterpret_cast<const double2*>(diag), N, 0,
-                                                     dim, sg * per, (sg + 1) * per,
+                                                     dim, bnd[sg], bnd[sg + 1],
                                                      sg ? part : nullptr, part, 0, nullptr,
                                                      PD_LAYOUT_GLOBAL, ctx->stream);
             if (e != cudaSuccess) return cuda_fail(e, "gray segment launch");
         }
-        c_last = (segs - 1) * per;
-        PD_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->cols_ready[segs - 1], 0));
+        c_last = bnd[nseg - 1];
+        PD_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->cols_ready[nseg - 1], 0));
         PD_CUDA(cudaEventRecord(ctx->gathered, ctx->stream));
     } else {
         if (int rc = upload(ctx, ctx->g, g, bytes)) return rc;
