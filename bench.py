@@ -417,8 +417,8 @@ def run_ours(args) -> None:
 
 def side_configs(pd, dev, stream, sptr, peaks):
     """The other BASELINE configs on one GPU, device-resident, CUDA events, 3 warm-ups:
-    configs[3] (full N=12 decomposition, the metric's other size) and configs[1] (65,536
-    batched single strings at N=10)."""
+    configs[3] (full N=12 decomposition, the metric's other size), configs[1] (65,536 batched
+    single strings at N=10), configs[2] (full N=10 Hermitian) and configs[0] (full N=6)."""
     import numpy as np
     import torch
 
@@ -455,7 +455,24 @@ def side_configs(pd, dev, stream, sptr, peaks):
     ms = ev_time(lambda: pd.device.coeff_batch(nq, g.data_ptr(), ns.data_ptr(), 65536, False, o.data_ptr(), sptr), 20)
     res["n10_strings"] = {"config": "BASELINE configs[1]: 65,536 random strings of an N=10 matrix",
                           "value": 65536 / (ms / 1e3), "unit": "strings/s", "ms_per_step": ms,
-                          "l2_gbs": 65536 * 16.0 * 2**nq / (ms / 1e3) / 1e9}
+                          "kernel": "K3b: bucketed by X-mask, one CTA per bucket over its staged diagonal"}
+    # configs[2]: full N=10 decomposition of a Hermitian matrix (imaginary parts ~0)
+    a = gen.standard_normal((2**nq, 2**nq)) + 1j * gen.standard_normal((2**nq, 2**nq))
+    h = torch.from_numpy((a + a.conj().T) / 2).to(dev)
+    out = torch.empty(4**nq, dtype=torch.complex128, device=dev)
+    scr = torch.empty(4**nq, dtype=torch.complex128, device=dev)
+    ms = ev_time(lambda: pd.device.decompose(nq, h.data_ptr(), out.data_ptr(), scr.data_ptr(), "gray", sptr), 20)
+    res["n10_hermitian_full"] = {"config": "BASELINE configs[2]: full N=10 decomposition of (A+A^H)/2",
+                                 "value": 4**nq / (ms / 1e3), "unit": UNIT, "ms_per_step": ms,
+                                 "max_abs_imag": float(torch.max(torch.abs(out.imag)))}
+    # configs[0]: full N=6 decomposition (latency of one small call on the device)
+    nq = 6
+    g6 = torch.from_numpy(gen.standard_normal((64, 64)) + 1j * gen.standard_normal((64, 64))).to(dev)
+    o6 = torch.empty(4**nq, dtype=torch.complex128, device=dev)
+    s6 = torch.empty(4**nq, dtype=torch.complex128, device=dev)
+    ms = ev_time(lambda: pd.device.decompose(nq, g6.data_ptr(), o6.data_ptr(), s6.data_ptr(), "gray", sptr), 50)
+    res["n6_full"] = {"config": "BASELINE configs[0]: full N=6 decomposition", "value": 4**nq / (ms / 1e3),
+                      "unit": UNIT, "ms_per_step": ms}
     return res
 
 

@@ -442,6 +442,7 @@ struct WhtPipe {
     cudaStream_t side[2] = {nullptr, nullptr};
     cudaEvent_t fork = nullptr, join[2] = {nullptr, nullptr};
     bool ok = false;
+    std::mutex issue;  // one fork/chunks/join sequence at a time (the events are shared)
 };
 
 WhtPipe& wht_pipe(int dev) {
@@ -541,6 +542,7 @@ cudaError_t launch_wht_from_matrix(const double2* G, unsigned N, uint64_t x0, ui
     WhtPipe& p = wht_pipe(dev);
     if (!p.ok) return cudaErrorInitializationError;
     const uint64_t dim = 1ull << N;
+    std::lock_guard<std::mutex> lk(p.issue);
     cudaError_t e = cudaEventRecord(p.fork, stream);
     for (int k = 0; e == cudaSuccess && k < 2; ++k) e = cudaStreamWaitEvent(p.side[k], p.fork, 0);
     for (uint64_t c = 0; e == cudaSuccess && c < x_count / S; ++c) {
