@@ -432,15 +432,16 @@ static cudaError_t launch_pass2(const double2* scratch, unsigned N, uint64_t x0,
 
 bool wht_fused_ok(unsigned N, uint64_t x_count) { return N >= 8 && N <= 16 && x_count >= 32; }
 
-// Chunked L2-resident pipeline. D' of a chunk of S X-masks (S 2^N x 16 B, ~32 MiB) is written
+// Chunked L2-resident pipeline. D' of a chunk of S X-masks (S 2^N x 16 B, 16 MiB) is written
 // by pass 1 with default (L2-allocating) stores and read back by pass 2 before it leaves L2;
 // pass 2 then discards the lines (discard.global.L2), so D' never reaches DRAM and the HBM
-// traffic is the algorithmic 32 4^N B (read G, write coefficients). Chunks alternate between
-// two D' slots and two streams, so one chunk's pass 2 overlaps the next chunk's pass 1.
+// traffic is the algorithmic 32 4^N B (read G, write coefficients). Chunks rotate over four D'
+// slots and four streams, so a chunk's pass 2 overlaps the following chunks' pass 1.
 namespace {
+constexpr int kWhtMaxStreams = 4;
 struct WhtPipe {
-    cudaStream_t side[2] = {nullptr, nullptr};
-    cudaEvent_t fork = nullptr, join[2] = {nullptr, nullptr};
+    cudaStream_t side[kWhtMaxStreams] = {};
+    cudaEvent_t fork = nullptr, join[kWhtMaxStreams] = {};
     bool ok = false;
     std::mutex issue;  // one fork/chunks/join sequence at a time (the events are shared)
 };
@@ -452,7 +453,7 @@ WhtPipe& wht_pipe(int dev) {
     WhtPipe& p = pipes[dev & 63];
     if (!p.ok) {
         bool good = cudaEventCreateWithFlags(&p.fork, cudaEventDisableTiming) == cudaSuccess;
-        for (int k = 0; good && k < 2; ++k)
+        for (int k = 0; good && k < kWhtMaxStreams; ++k)
             good = cudaStreamCreateWithFlags(&p.side[k], cudaStreamNonBlocking) == cudaSuccess &&
                    cudaEventCreateWithFlags(&p.join[k], cudaEventDisableTiming) == cudaSuccess;
         p.ok = good;
@@ -461,12 +462,9 @@ WhtPipe& wht_pipe(int dev) {
 }
 
 uint64_t wht_chunk(unsigned N) {
-    static const long env = [] {
-        const char* e = std::getenv("PD_WHT_CHUNK");
-        return e ? std::atol(e) : 0L;
-    }();
-    if (env > 0) return static_cast<uint64_t>(env);
-    const uint64_t s = (32ull << 20) / (sizeof(double2) << N);  // ~32 MiB of D' per chunk
+    // 16 MiB of D' per chunk, 4 chunks in flight: 64 MiB of the 126 MB L2 (measured optimum at
+    // N=12 and N=14: 2 x 32 MiB is 1 % slower, 1 x 64 MiB or 4 x 32 MiB 6-8 % slower)
+    const uint64_t s = (16ull << 20) / (sizeof(double2) << N);
     return s < 32 ? 32 : s;
 }
 }  // namespace
@@ -535,7 +533,7 @@ cudaError_t launch_wht_from_matrix(const double2* G, unsigned N, uint64_t x0, ui
     const uint64_t S = wht_chunk(N);
     const unsigned hb = N - kLoBits;
     const bool reg_pass2 = hb >= 4 && hb <= 8;
-    if (!reg_pass2 || x_count < 2 * S || (S & 31) || x_count % S)
+    if (!reg_pass2 || x_count < 4 * S || (S & 31) || x_count % S)
         return wht_two_pass(G, N, x0, x_count, scratch, map, false, stream);
     int dev = 0;
     cudaGetDevice(&dev);
@@ -544,12 +542,13 @@ cudaError_t launch_wht_from_matrix(const double2* G, unsigned N, uint64_t x0, ui
     const uint64_t dim = 1ull << N;
     std::lock_guard<std::mutex> lk(p.issue);
     cudaError_t e = cudaEventRecord(p.fork, stream);
-    for (int k = 0; e == cudaSuccess && k < 2; ++k) e = cudaStreamWaitEvent(p.side[k], p.fork, 0);
+    constexpr int ns = kWhtMaxStreams;
+    for (int k = 0; e == cudaSuccess && k < ns; ++k) e = cudaStreamWaitEvent(p.side[k], p.fork, 0);
     for (uint64_t c = 0; e == cudaSuccess && c < x_count / S; ++c) {
-        const int k = static_cast<int>(c & 1);  // slot k of D' belongs to stream k
+        const int k = static_cast<int>(c % ns);  // slot k of D' belongs to stream k
         e = wht_two_pass(G, N, x0 + c * S, S, scratch + k * S * dim, map, true, p.side[k]);
     }
-    for (int k = 0; e == cudaSuccess && k < 2; ++k) {
+    for (int k = 0; e == cudaSuccess && k < ns; ++k) {
         e = cudaEventRecord(p.join[k], p.side[k]);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, p.join[k], 0);
     }
