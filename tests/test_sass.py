@@ -14,6 +14,7 @@ import pytest
 from conftest import ROOT
 
 OBJ = os.path.join(ROOT, "paper_2401_16378_b200", "csrc", "build", "pd_kernels.o")
+SEG_OBJ = os.path.join(ROOT, "paper_2401_16378_b200", "csrc", "build", "pd_k2seg.o")
 WHT_OBJ = os.path.join(ROOT, "paper_2401_16378_b200", "csrc", "build", "pd_wht.o")
 CUOBJDUMP = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
 
@@ -83,3 +84,15 @@ def test_no_local_memory_in_hot_kernels():
             name, stack, spills = m.group(1), int(m.group(2)), int(m.group(3))
             if "gray_xmask" in name or "wht_" in name or "diag_gather" in name:
                 assert spills == 0, (name, spills)
+
+
+def test_k2_segment_instantiation_is_separate_and_clean():
+    """The host pipeline's walk-segment K2 is compiled alone (pd_k2seg.cu, ptxas -O1) so it
+    cannot move the whole-walk kernel's schedule; it must still be the pure-DADD loop."""
+    seg = "_ZN3pdb17gray_xmask_kernelILi4ELb1ELb0EEEvNS_8K2ParamsE"
+    listing = subprocess.run([CUOBJDUMP, "-sass", OBJ], capture_output=True, text=True).stdout
+    assert seg not in listing, "segment instantiation leaked into pd_kernels.o"
+    body = innermost_loop(sass_of(SEG_OBJ, seg))
+    ops = [b.split()[0] for b in body]
+    assert sum(o == "DADD" for o in ops) == 1024
+    assert not any(o.startswith(("LDL", "STL")) for o in ops)
