@@ -608,9 +608,10 @@ namespace {
 // p bits equal g. Its diagonals touch only the P tiles (row block t ^ g, column block t) of G,
 // so it uploads exactly those (1/P of G) straight from the host, runs K1+K2 (or the WHT) on
 // its block with the runs packed (PD_LAYOUT_RUNS), and downloads its 2^p runs straight to their
-// offsets of the host output: every transfer goes over the device's own host link and there is
-// no device-to-device traffic at all. The devices' work is issued asynchronously from this
-// thread and overlaps; results are bit-identical to one device.
+// offsets of the host output (in sub-blocks, overlapped with the compute of the next): every
+// transfer goes over the device's own host link and there is no device-to-device traffic at
+// all. The devices' work is issued asynchronously from this thread and overlaps; results are
+// bit-identical to one device.
 int decompose_multi(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_path path) {
     const uint64_t P = ctx->subs.size();
     const unsigned p = static_cast<unsigned>(__builtin_ctzll(P));
@@ -635,16 +636,32 @@ int decompose_multi(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pa
             PD_CUDA(cudaMemcpy2DAsync(gd + off, dim * sizeof(double2), g + off, dim * sizeof(double2),
                                       B * sizeof(double2), B, cudaMemcpyHostToDevice, s->stream));
         }
-        if (int rc = pd_shard_coeffs_device(N, gd, d * B, B, p, static_cast<double*>(s->out),
-                                            PD_LAYOUT_RUNS, s->scratch, path, s->stream))
-            return rc;
-        for (uint64_t r = 0; r < P; ++r)
-            PD_CUDA(cudaMemcpyAsync(out + 2 * pd_run_offset(N, p, d, r),
-                                    static_cast<double*>(s->out) + 2 * r * run_len,
-                                    run_len * sizeof(double2), cudaMemcpyDeviceToHost, s->stream));
+        // Q sub-blocks of the device's X-masks, each downloaded while the next computes. A
+        // sub-block writes into the device's packed runs (rb = p, the fast run-pointer K2); its
+        // coefficients there are P Q contiguous pieces of 4^(N-p-q): z's top p bits r select the
+        // run, the next q digits (from x bits s and z bits u) the piece.
+        const unsigned q = (B >= 512) ? 2u : (B >= 256 ? 1u : 0u);
+        const uint64_t Q = 1ull << q, Bs = B >> q;
+        const uint64_t piece = 1ull << (2 * (N - p - q));
+        double* so = static_cast<double*>(s->out);
+        for (uint64_t sb_i = 0; sb_i < Q; ++sb_i) {
+            if (int rc = pd_shard_coeffs_device(N, gd, d * B + sb_i * Bs, Bs, p, so, PD_LAYOUT_RUNS,
+                                                s->scratch, path, s->stream))
+                return rc;
+            PD_CUDA(cudaEventRecord(s->block_done[sb_i], s->stream));
+            PD_CUDA(cudaStreamWaitEvent(s->d2h, s->block_done[sb_i], 0));
+            for (uint64_t r = 0; r < P; ++r)
+                for (uint64_t u = 0; u < Q; ++u) {
+                    const uint64_t host_off = pd_run_offset(N, p + q, d * Q + sb_i, r * Q + u);
+                    const uint64_t dev_off = r * run_len + (pd_run_offset(q, q, sb_i, u) << (2 * (N - p - q)));
+                    PD_CUDA(cudaMemcpyAsync(out + 2 * host_off, so + 2 * dev_off, piece * sizeof(double2),
+                                            cudaMemcpyDeviceToHost, s->d2h));
+                }
+        }
     }
     for (pd_ctx* s : ctx->subs) {
         if (int rc = bind(s)) return rc;
+        PD_CUDA(cudaStreamSynchronize(s->d2h));
         PD_CUDA(cudaStreamSynchronize(s->stream));
     }
     return bind(ctx);

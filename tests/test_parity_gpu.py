@@ -441,7 +441,7 @@ def test_array_like_inputs_are_coerced_like_the_reference_binding(pd, cuda, port
 
 
 @pytest.mark.parametrize("devices", [[0, 0], [0, 0, 0, 0], [0] * 8])
-@pytest.mark.parametrize("nq,path", [(9, "gray"), (12, "gray"), (12, "wht")])
+@pytest.mark.parametrize("nq,path", [(9, "gray"), (12, "gray"), (12, "wht"), (13, "gray")])
 def test_multi_device_context_matches_one_device(pd, cuda, devices, nq, path):
     """pd_ctx_create_multi on a list that repeats device 0: every virtual device gets its own
     streams and buffers (left uninitialised), uploads only the tiles (t ^ g, t) of G its
