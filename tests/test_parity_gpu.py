@@ -451,3 +451,29 @@ def test_multi_device_context_matches_one_device(pd, cuda, devices, nq, path):
     want = pd.decompose(g, path=path)
     got = pd.decompose(g, path=path, devices=devices)
     assert np.array_equal(got, want)
+
+
+def test_random_sizes_paths_and_batches(pd, cuda, port):
+    """Hypothesis-drawn sizes, paths, matrices and string batches against the oracle: Gray and
+    naive paths and every batched string bit for bit, the WHT path within the tolerance."""
+    from hypothesis import HealthCheck, given, settings
+    from hypothesis import strategies as st
+
+    @settings(max_examples=30, deadline=None, suppress_health_check=list(HealthCheck))
+    @given(st.integers(1, 11), st.sampled_from(["gray", "wht", "naive"]), st.integers(0, 2**32 - 1),
+           st.integers(0, 5000))
+    def check(nq, path, seed, count):
+        rng = np.random.default_rng(seed)
+        g = rng.standard_normal((2**nq, 2**nq)) + 1j * rng.standard_normal((2**nq, 2**nq))
+        if rng.random() < 0.3:  # small integers: every path is exact
+            g = rng.integers(-4, 5, (2**nq, 2**nq)) + 1j * rng.integers(-4, 5, (2**nq, 2**nq))
+        want = port.decompose(g)
+        got = pd.decompose(g, path=path)
+        if path == "wht":
+            assert np.max(np.abs(got - want)) <= 1e-11 * max(np.max(np.abs(want)), 1e-300)
+        else:
+            assert same_values(got, want)
+        ns = rng.integers(0, 4**nq, count).astype(np.uint64)
+        assert same_values(pd.coefficients(g, ns), want[ns.astype(np.int64)])
+
+    check()
