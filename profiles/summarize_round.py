@@ -44,6 +44,9 @@ def main():
         ("N=12 full (configs[3])", f"{sc['n12_full_gray']['ms_per_step']:.3f} ms, "
                                    f"{100 * sc['n12_full_gray']['fp64_frac_incl_k1']:.1f} % of FP64 peak incl. K1"),
         ("N=10 65,536 strings (configs[1])", f"{1e3 * sc['n10_strings']['ms_per_step']:.1f} us"),
+        ("N=10 Hermitian full (configs[2])", f"{1e3 * sc['n10_hermitian_full']['ms_per_step']:.1f} us, "
+                                             f"max |Im c| = {sc['n10_hermitian_full']['max_abs_imag']:.1e}"),
+        ("N=6 full (configs[0])", f"{1e3 * sc['n6_full']['ms_per_step']:.1f} us"),
         ("CPU reference (oracle/_ref, coeff_fast)",
          f"{cb['value']:.0f} coeff/s, {cb['cores']} threads, {cb['sample']}; GPU/CPU = {b['value'] / cb['value']:.0f}x"),
         ("clocks during the timed region", f"{b['clocks']['sm_mhz']:.0f} / {b['clocks']['sm_max_mhz']:.0f} MHz, "
@@ -63,7 +66,7 @@ def main():
             "## Launch list of the default bench command (cold-cache, serialised — compare shares)", "",
             launches(os.path.join(HERE, "r01_launches_N14_bench.csv")), "",
             "(`gray_xmask_kernel<4,1,0>` is the segmented K2 of the pipelined host path inside the e2e "
-            "measurement; `<4,0,0>` the device-resident one; the WHT kernels run once per 128-X-mask chunk, "
+            "measurement; `<4,0,0>` the device-resident one; the WHT kernels run once per 64-X-mask chunk (16 MiB of D'), "
             "the strings kernels once per configs[1] batch.)", "",
             "## Full-set captures", "",
             report(os.path.join(HERE, "r01_prof_gray_N14.ncu-rep")), "",
