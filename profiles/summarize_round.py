@@ -45,7 +45,7 @@ def main():
                                    f"{100 * sc['n12_full_gray']['fp64_frac_incl_k1']:.1f} % of FP64 peak incl. K1"),
         ("N=10 65,536 strings (configs[1])", f"{1e3 * sc['n10_strings']['ms_per_step']:.1f} us"),
         ("N=10 Hermitian full (configs[2])", f"{1e3 * sc['n10_hermitian_full']['ms_per_step']:.1f} us, "
-                                             f"max |Im c| = {sc['n10_hermitian_full']['max_abs_imag']:.1e}"),
+                                             f"max abs(Im c) = {sc['n10_hermitian_full']['max_abs_imag']:.1e}"),
         ("N=6 full (configs[0])", f"{1e3 * sc['n6_full']['ms_per_step']:.1f} us"),
         ("CPU reference (oracle/_ref, coeff_fast)",
          f"{cb['value']:.0f} coeff/s, {cb['cores']} threads, {cb['sample']}; GPU/CPU = {b['value'] / cb['value']:.0f}x"),

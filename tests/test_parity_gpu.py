@@ -477,3 +477,34 @@ def test_random_sizes_paths_and_batches(pd, cuda, port):
         assert same_values(pd.coefficients(g, ns), want[ns.astype(np.int64)])
 
     check()
+
+
+def test_concurrent_callers(pd, cuda, port):
+    """Host threads decomposing at once (one context per device, serialised by the C++ layer;
+    the shared WHT stream pipeline and lazily set kernel attributes must not race)."""
+    import threading
+    rng = np.random.default_rng(77)
+    mats = [normal_matrix(rng, nq) for nq in (6, 9, 10, 11)]
+    want = [port.decompose(g) for g in mats]
+    errors = []
+
+    def work(k):
+        try:
+            for rep in range(3):
+                g = mats[(k + rep) % len(mats)]
+                w = want[(k + rep) % len(mats)]
+                path = ("gray", "wht", "naive")[(k + rep) % 3]
+                got = pd.decompose(g, path=path)
+                ok = (np.max(np.abs(got - w)) <= 1e-11 * np.max(np.abs(w))) if path == "wht" \
+                    else same_values(got, w)
+                if not ok:
+                    errors.append((k, rep, path))
+        except Exception as exc:  # pragma: no cover - reported below
+            errors.append((k, repr(exc)))
+
+    threads = [threading.Thread(target=work, args=(k,)) for k in range(6)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
