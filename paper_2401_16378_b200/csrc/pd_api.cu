@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "pd_api.h"
+#include "pd_device.cuh"
 #include "pd_kernels.h"
 
 namespace {
@@ -124,6 +125,8 @@ struct pd_ctx {
     void* ns = nullptr;
     size_t ns_bytes = 0;
     std::vector<pd_ctx*> subs;       // multi-device context: one sub-context per listed device
+    void* stage = nullptr;           // pinned host staging (single-string diagonal)
+    size_t stage_bytes = 0;
 
     int ensure(void** p, size_t* have, size_t need) {
         if (*have >= need) return PD_OK;
@@ -214,6 +217,8 @@ int pd_ctx_destroy(pd_ctx* ctx) {
     if (!ctx) return PD_OK;
     for (pd_ctx* sub : ctx->subs) pd_ctx_destroy(sub);
     ctx->subs.clear();
+    if (ctx->stage) cudaFreeHost(ctx->stage);
+    ctx->stage = nullptr;
     cudaSetDevice(ctx->device);
     for (cudaStream_t s : {ctx->stream, ctx->stream2, ctx->d2h, ctx->h2d})
         if (s) cudaStreamSynchronize(s);
@@ -713,18 +718,33 @@ int pd_coeff(pd_ctx* ctx, unsigned N, const double* g, uint64_t n, int slow, dou
     if (int rc = check_qubits(N)) return rc;
     if (int rc = check_index(N, n)) return rc;
     if (int rc = bind(ctx)) return rc;
-    const size_t gbytes = elems(N) * sizeof(double2);
-    if (int rc = ctx->ensure(&ctx->g, &ctx->g_bytes, gbytes)) return rc;
-    if (int rc = ctx->ensure(&ctx->ns, &ctx->ns_bytes, sizeof(uint64_t))) return rc;
+    // one string reads one XOR-diagonal: gather its 2^N elements on the host (16 KiB at N=10,
+    // 256 KiB at N=14) instead of uploading the whole matrix, then walk it in the reference's
+    // order on the device (K3 over the compact diagonal; bit-identical to the full-matrix walk)
+    const uint64_t dim = 1ull << N;
+    const uint64_t x = pdb::xmask_of(n);
+    const size_t dbytes = dim * sizeof(double2) + sizeof(uint64_t);
+    if (ctx->stage_bytes < dbytes) {
+        if (ctx->stage) cudaFreeHost(ctx->stage);
+        ctx->stage = nullptr;
+        ctx->stage_bytes = 0;
+        PD_CUDA(cudaHostAlloc(&ctx->stage, dbytes, cudaHostAllocDefault));
+        ctx->stage_bytes = dbytes;
+    }
+    double* d = static_cast<double*>(ctx->stage);
+    for (uint64_t i = 0; i < dim; ++i) {
+        const double* e = g + 2 * ((i ^ x) * dim + i);
+        d[2 * i] = e[0];
+        d[2 * i + 1] = e[1];
+    }
+    std::memcpy(d + 2 * dim, &n, sizeof(n));
+    if (int rc = ctx->ensure(&ctx->g, &ctx->g_bytes, dbytes)) return rc;
     if (int rc = ctx->ensure(&ctx->out, &ctx->out_bytes, sizeof(double2))) return rc;
-    if (int rc = upload(ctx, ctx->g, g, gbytes)) return rc;
-    if (int rc = upload(ctx, ctx->ns, &n, sizeof(uint64_t))) return rc;
-    // the pageable source of the 8-byte index must stay valid until the copy runs
-    PD_CUDA(cudaStreamSynchronize(ctx->stream));
-    if (int rc = pd_coeff_batch_device(N, static_cast<const double*>(ctx->g),
-                                       static_cast<const uint64_t*>(ctx->ns), 1, slow,
-                                       static_cast<double*>(ctx->out), ctx->stream))
-        return rc;
+    PD_CUDA(cudaMemcpyAsync(ctx->g, d, dbytes, cudaMemcpyHostToDevice, ctx->stream));
+    const double2* dd = static_cast<const double2*>(ctx->g);
+    cudaError_t e = pdb::launch_walk_diag(dd, N, reinterpret_cast<const uint64_t*>(dd + dim), slow != 0,
+                                          static_cast<double2*>(ctx->out), ctx->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "walk launch");
     PD_CUDA(cudaMemcpyAsync(out, ctx->out, sizeof(double2), cudaMemcpyDeviceToHost, ctx->stream));
     PD_CUDA(cudaStreamSynchronize(ctx->stream));
     return PD_OK;

@@ -14,6 +14,7 @@
 
 #include <atomic>
 #include <cstdint>
+#include <type_traits>
 
 #include "pd_device.cuh"
 #include "pd_k2.cuh"
@@ -236,7 +237,7 @@ __device__ __forceinline__ void walk_block(const double2* __restrict__ G, uint64
 template <bool SLOW, int B>
 __global__ void __launch_bounds__(128)
     walk_kernel(const double2* __restrict__ G, unsigned N, const uint64_t* __restrict__ ns,
-                uint64_t count, double2* __restrict__ out, double scale) {
+                uint64_t count, double2* __restrict__ out, double scale, uint64_t row_stride) {
     const uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (k >= count) return;
     const uint64_t n = ns ? ns[k] : k;
@@ -248,27 +249,121 @@ __global__ void __launch_bounds__(128)
     const uint64_t zh = z >> B;
     for (uint64_t kh = 0; kh < nblocks; kh += 2) {
         if (kh != 0) sgn_hi ^= static_cast<unsigned>((zh >> (__ffsll(static_cast<long long>(kh)) - 1)) & 1) << 31;
-        walk_block<SLOW, B, false>(G, dim, x, z, gray(kh), sgn_hi, sr, si);
+        walk_block<SLOW, B, false>(G, row_stride, x, z, gray(kh), sgn_hi, sr, si);
         if (kh + 1 < nblocks) {
             sgn_hi ^= static_cast<unsigned>((zh >> (__ffsll(static_cast<long long>(kh + 1)) - 1)) & 1) << 31;
-            walk_block<SLOW, B, true>(G, dim, x, z, gray(kh + 1), sgn_hi, sr, si);
+            walk_block<SLOW, B, true>(G, row_stride, x, z, gray(kh + 1), sgn_hi, sr, si);
         }
     }
     const unsigned ph = (3u * static_cast<unsigned>(__popcll(x & z))) & 3u;
     out[k] = apply_phase(ph, sr, si, scale);
 }
 
+// row_stride = 2^N walks G itself; row_stride = 0 walks a compact diagonal D[i] = G[i ^ x][i]
+// of the (single) string's X-mask
 template <bool SLOW>
 static cudaError_t launch_walk_t(const double2* G, unsigned N, const uint64_t* ns, uint64_t count,
-                                 double2* out, cudaStream_t stream) {
+                                 double2* out, uint64_t row_stride, cudaStream_t stream) {
     const double scale = 1.0 / static_cast<double>(1ull << N);
     const unsigned threads = 128;
     const uint64_t grid = (count + threads - 1) / threads;
     switch (N < 3 ? N : 3) {
-        case 1: walk_kernel<SLOW, 1><<<static_cast<unsigned>(grid), threads, 0, stream>>>(G, N, ns, count, out, scale); break;
-        case 2: walk_kernel<SLOW, 2><<<static_cast<unsigned>(grid), threads, 0, stream>>>(G, N, ns, count, out, scale); break;
-        default: walk_kernel<SLOW, 3><<<static_cast<unsigned>(grid), threads, 0, stream>>>(G, N, ns, count, out, scale); break;
+        case 1: walk_kernel<SLOW, 1><<<static_cast<unsigned>(grid), threads, 0, stream>>>(G, N, ns, count, out, scale, row_stride); break;
+        case 2: walk_kernel<SLOW, 2><<<static_cast<unsigned>(grid), threads, 0, stream>>>(G, N, ns, count, out, scale, row_stride); break;
+        default: walk_kernel<SLOW, 3><<<static_cast<unsigned>(grid), threads, 0, stream>>>(G, N, ns, count, out, scale, row_stride); break;
     }
+    return count_launch();
+}
+
+// One string over its gathered diagonal, latency-optimised: the walk is one dependent chain per
+// component, so a single thread sums while the CTA streams the diagonal through two shared-
+// memory stages (cp.async) in walk order (an aligned run of C Gray steps covers the contiguous
+// range [gray(c) C, gray(c) C + C)). Same order, same result as walk_kernel, bit for bit.
+constexpr int kW1Threads = 256;
+constexpr unsigned kW1ChunkLog = 12;  // 4096 elements = 64 KiB per stage
+
+__global__ void __launch_bounds__(kW1Threads)
+    walk_one_kernel(const double2* __restrict__ D, unsigned N, const uint64_t* __restrict__ np,
+                    double2* __restrict__ out, double scale) {
+    extern __shared__ __align__(16) double2 st[];  // 2 stages
+    const uint64_t dim = 1ull << N;
+    const unsigned clog = N < kW1ChunkLog ? N : kW1ChunkLog;
+    const uint64_t C = 1ull << clog, nchunks = dim >> clog;
+    const uint64_t n = *np;
+    const uint64_t x = xmask_of(n), z = zmask_of(n);
+    auto stage_in = [&](uint64_t c, unsigned s) {
+        const double2* src = D + (gray(c) << clog);
+        for (uint64_t i = threadIdx.x; i < C; i += kW1Threads) {
+            const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(st + s * C + i));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src + i) : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    stage_in(0, 0);
+    double sr = 0.0, si = 0.0;
+    unsigned sgn_hi = 0;
+    const uint64_t zh = z >> 4;
+    const unsigned zl = static_cast<unsigned>(z) & 15u;
+    unsigned sw[16];
+#pragma unroll
+    for (int il = 0; il < 16; ++il) sw[il] = static_cast<unsigned>(__popc(static_cast<unsigned>(il) & zl) & 1) << 31;
+    for (uint64_t c = 0; c < nchunks; ++c) {
+        if (c + 1 < nchunks) {
+            stage_in(c + 1, (c + 1) & 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const double2* base = st + (c & 1) * C;
+            const uint64_t kh0 = c << (clog - 4 < 64 ? clog - 4 : 0);
+            auto block = [&](uint64_t kh, auto odd) {
+                constexpr unsigned kOdd = decltype(odd)::value ? 8u : 0u;
+                if (kh != 0) sgn_hi ^= static_cast<unsigned>((zh >> (__ffsll(static_cast<long long>(kh)) - 1)) & 1) << 31;
+                const double2* blk = base + ((gray(kh) << 4) & (C - 1));
+                double2 e[16];
+#pragma unroll
+                for (int p = 0; p < 16; ++p) e[p] = blk[cgray(p) ^ kOdd];
+#pragma unroll
+                for (int p = 0; p < 16; ++p) {
+                    const unsigned sgn = sgn_hi ^ sw[cgray(p) ^ kOdd];
+                    sr += flip_sign(e[p].x, sgn);
+                    si += flip_sign(e[p].y, sgn);
+                }
+            };
+            const uint64_t nb = C >> 4;  // 1 (N = 4) or even
+            for (uint64_t b = 0; b < nb; b += 2) {
+                block(kh0 + b, std::false_type{});
+                if (b + 1 < nb) block(kh0 + b + 1, std::true_type{});
+            }
+        }
+        __syncthreads();  // the stage is refilled next iteration
+    }
+    if (threadIdx.x == 0) {
+        const unsigned ph = (3u * static_cast<unsigned>(__popcll(x & z))) & 3u;
+        *out = apply_phase(ph, sr, si, scale);
+    }
+}
+
+cudaError_t launch_walk_diag(const double2* D, unsigned N, const uint64_t* n, bool slow, double2* out,
+                             cudaStream_t stream) {
+    if (slow || N < 4)  // coeff_slow semantics, and sizes below one 16-element block
+        return slow ? launch_walk_t<true>(D, N, n, 1, out, 0, stream)
+                    : launch_walk_t<false>(D, N, n, 1, out, 0, stream);
+    static std::atomic<uint64_t> attr_set{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const size_t smem = 2 * sizeof(double2) << kW1ChunkLog;
+    if (!(attr_set.load() >> dev & 1)) {
+        const cudaError_t e = cudaFuncSetAttribute(walk_one_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        attr_set.fetch_or(1ull << dev);
+    }
+    const unsigned clog = N < kW1ChunkLog ? N : kW1ChunkLog;
+    walk_one_kernel<<<1, kW1Threads, 2 * sizeof(double2) << clog, stream>>>(
+        D, N, n, out, 1.0 / static_cast<double>(1ull << N));
     return count_launch();
 }
 
@@ -277,8 +372,9 @@ cudaError_t launch_walk(const double2* G, unsigned N, const uint64_t* ns, uint64
     if (count == 0) return cudaSuccess;
     if (!slow && ns != nullptr && strings_grouped_ok(N, count))
         return launch_strings_grouped(G, N, ns, count, out, stream);
-    return slow ? launch_walk_t<true>(G, N, ns, count, out, stream)
-                : launch_walk_t<false>(G, N, ns, count, out, stream);
+    const uint64_t dim = 1ull << N;
+    return slow ? launch_walk_t<true>(G, N, ns, count, out, dim, stream)
+                : launch_walk_t<false>(G, N, ns, count, out, dim, stream);
 }
 
 // ============================================================================
