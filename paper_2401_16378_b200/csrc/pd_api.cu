@@ -8,6 +8,7 @@
 // There is no CPU path: without an sm_100 device every compute call is PD_ENODEV.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdarg>
 #include <cstdint>
 #include <cstdio>
@@ -699,6 +700,50 @@ int pd_coeff_batch(pd_ctx* ctx, unsigned N, const double* g, const uint64_t* ns,
     if (int rc = bind(ctx)) return rc;
     if (count == 0) return PD_OK;
     const size_t gbytes = elems(N) * sizeof(double2);
+    const uint64_t dim = 1ull << N;
+    // few X-masks among the strings (at most 2^N / 8): upload only their gathered diagonals
+    std::vector<uint64_t> xs(count);
+    for (uint64_t k = 0; k < count; ++k) xs[k] = pdb::xmask_of(ns[k]);
+    std::vector<uint64_t> uniq(xs);
+    std::sort(uniq.begin(), uniq.end());
+    uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
+    if (N >= 4 && uniq.size() * 8 <= dim) {
+        const uint64_t m = uniq.size();
+        const size_t dbytes = m * dim * sizeof(double2);
+        const size_t need = dbytes + count * (sizeof(uint64_t) + sizeof(uint32_t));
+        if (ctx->stage_bytes < need) {
+            if (ctx->stage) cudaFreeHost(ctx->stage);
+            ctx->stage = nullptr;
+            ctx->stage_bytes = 0;
+            PD_CUDA(cudaHostAlloc(&ctx->stage, need, cudaHostAllocDefault));
+            ctx->stage_bytes = need;
+        }
+        double* d = static_cast<double*>(ctx->stage);
+        for (uint64_t j = 0; j < m; ++j)
+            for (uint64_t i = 0; i < dim; ++i) {
+                const double* e = g + 2 * ((i ^ uniq[j]) * dim + i);
+                d[2 * (j * dim + i)] = e[0];
+                d[2 * (j * dim + i) + 1] = e[1];
+            }
+        uint64_t* nsh = reinterpret_cast<uint64_t*>(static_cast<char*>(ctx->stage) + dbytes);
+        uint32_t* slot = reinterpret_cast<uint32_t*>(nsh + count);
+        std::memcpy(nsh, ns, count * sizeof(uint64_t));
+        for (uint64_t k = 0; k < count; ++k)
+            slot[k] = static_cast<uint32_t>(std::lower_bound(uniq.begin(), uniq.end(), xs[k]) - uniq.begin());
+        if (int rc = ctx->ensure(&ctx->g, &ctx->g_bytes, need)) return rc;
+        if (int rc = ctx->ensure(&ctx->out, &ctx->out_bytes, count * sizeof(double2))) return rc;
+        PD_CUDA(cudaMemcpyAsync(ctx->g, ctx->stage, need, cudaMemcpyHostToDevice, ctx->stream));
+        const char* base = static_cast<const char*>(ctx->g);
+        cudaError_t e = pdb::launch_walk_slots(
+            reinterpret_cast<const double2*>(base), N, reinterpret_cast<const uint64_t*>(base + dbytes),
+            reinterpret_cast<const uint32_t*>(base + dbytes + count * sizeof(uint64_t)), count,
+            static_cast<double2*>(ctx->out), ctx->stream);
+        if (e != cudaSuccess) return cuda_fail(e, "walk launch");
+        PD_CUDA(cudaMemcpyAsync(out, ctx->out, count * sizeof(double2), cudaMemcpyDeviceToHost,
+                                ctx->stream));
+        PD_CUDA(cudaStreamSynchronize(ctx->stream));
+        return PD_OK;
+    }
     if (int rc = ctx->ensure(&ctx->g, &ctx->g_bytes, gbytes)) return rc;
     if (int rc = ctx->ensure(&ctx->ns, &ctx->ns_bytes, count * sizeof(uint64_t))) return rc;
     if (int rc = ctx->ensure(&ctx->out, &ctx->out_bytes, count * sizeof(double2))) return rc;

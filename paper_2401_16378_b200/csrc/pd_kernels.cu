@@ -237,9 +237,11 @@ __device__ __forceinline__ void walk_block(const double2* __restrict__ G, uint64
 template <bool SLOW, int B>
 __global__ void __launch_bounds__(128)
     walk_kernel(const double2* __restrict__ G, unsigned N, const uint64_t* __restrict__ ns,
-                uint64_t count, double2* __restrict__ out, double scale, uint64_t row_stride) {
+                uint64_t count, double2* __restrict__ out, double scale, uint64_t row_stride,
+                const uint32_t* __restrict__ slot) {
     const uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (k >= count) return;
+    if (slot) G += static_cast<uint64_t>(slot[k]) << N;  // compact diagonals, one per X-mask
     const uint64_t n = ns ? ns[k] : k;
     const uint64_t dim = 1ull << N;
     const uint64_t x = xmask_of(n), z = zmask_of(n);
@@ -263,16 +265,23 @@ __global__ void __launch_bounds__(128)
 // of the (single) string's X-mask
 template <bool SLOW>
 static cudaError_t launch_walk_t(const double2* G, unsigned N, const uint64_t* ns, uint64_t count,
-                                 double2* out, uint64_t row_stride, cudaStream_t stream) {
+                                 double2* out, uint64_t row_stride, cudaStream_t stream,
+                                 const uint32_t* slot = nullptr) {
     const double scale = 1.0 / static_cast<double>(1ull << N);
     const unsigned threads = 128;
     const uint64_t grid = (count + threads - 1) / threads;
     switch (N < 3 ? N : 3) {
-        case 1: walk_kernel<SLOW, 1><<<static_cast<unsigned>(grid), threads, 0, stream>>>(G, N, ns, count, out, scale, row_stride); break;
-        case 2: walk_kernel<SLOW, 2><<<static_cast<unsigned>(grid), threads, 0, stream>>>(G, N, ns, count, out, scale, row_stride); break;
-        default: walk_kernel<SLOW, 3><<<static_cast<unsigned>(grid), threads, 0, stream>>>(G, N, ns, count, out, scale, row_stride); break;
+        case 1: walk_kernel<SLOW, 1><<<static_cast<unsigned>(grid), threads, 0, stream>>>(G, N, ns, count, out, scale, row_stride, slot); break;
+        case 2: walk_kernel<SLOW, 2><<<static_cast<unsigned>(grid), threads, 0, stream>>>(G, N, ns, count, out, scale, row_stride, slot); break;
+        default: walk_kernel<SLOW, 3><<<static_cast<unsigned>(grid), threads, 0, stream>>>(G, N, ns, count, out, scale, row_stride, slot); break;
     }
     return count_launch();
+}
+
+cudaError_t launch_walk_slots(const double2* D, unsigned N, const uint64_t* ns, const uint32_t* slot,
+                              uint64_t count, double2* out, cudaStream_t stream) {
+    if (count == 0) return cudaSuccess;
+    return launch_walk_t<false>(D, N, ns, count, out, 0, stream, slot);
 }
 
 // One string over its gathered diagonal, latency-optimised: the walk is one dependent chain per

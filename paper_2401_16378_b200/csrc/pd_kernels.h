@@ -63,6 +63,9 @@ cudaError_t launch_recompose_scatter(const double2* rows, unsigned N, double2* G
                                      cudaStream_t stream);
 
 // K0/K3: one thread per tensor number (ns == nullptr: n = 0..count-1)
+// K3 over compact diagonals: string k walks D + slot[k] 2^N (its X-mask's gathered diagonal)
+cudaError_t launch_walk_slots(const double2* D, unsigned N, const uint64_t* ns, const uint32_t* slot,
+                              uint64_t count, double2* out, cudaStream_t stream);
 // K3 for one string over its gathered diagonal D[i] = G[i ^ x][i] (2^N entries)
 cudaError_t launch_walk_diag(const double2* D, unsigned N, const uint64_t* n, bool slow, double2* out,
                              cudaStream_t stream);

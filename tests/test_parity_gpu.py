@@ -508,3 +508,17 @@ def test_concurrent_callers(pd, cuda, port):
     for t in threads:
         t.join()
     assert not errors, errors
+
+
+@pytest.mark.parametrize("nq,count,n_x", [(8, 50, 3), (12, 200, 7), (14, 64, 64)])
+def test_sparse_batches_use_gathered_diagonals(pd, cuda, port, nq, count, n_x):
+    """Batches whose strings share few X-masks upload only those diagonals (pd_coeff_batch);
+    every value must still equal the oracle bit for bit, duplicates and all."""
+    rng = np.random.default_rng(count)
+    g = port.random_matrix(nq, 99 + nq) if nq == 14 else normal_matrix(rng, nq)
+    xs = rng.choice(2**nq, n_x, replace=False)
+    zs = rng.integers(0, 2**nq, count)
+    ns = np.array([_n(int(xs[k % n_x]), int(zs[k]), nq) for k in range(count)], dtype=np.uint64)
+    got = pd.coefficients(g, ns)
+    want = port.coeff_batch(g, ns)
+    assert same_values(got, want)
