@@ -387,6 +387,12 @@ int pd_recompose_device(unsigned N, const double* coeffs, double* g_out, void* s
     if (!coeffs || !g_out || !scratch) return fail(PD_EINVAL, "null buffer");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     double2* rows = static_cast<double2*>(scratch);
+    if (pdb::wht_inverse_ok(N)) {
+        cudaError_t e = pdb::launch_wht_inverse(reinterpret_cast<const double2*>(coeffs), N, rows,
+                                                reinterpret_cast<double2*>(g_out), s);
+        if (e != cudaSuccess) return cuda_fail(e, "recompose launch");
+        return PD_OK;
+    }
     cudaError_t e = pdb::launch_recompose_gather(reinterpret_cast<const double2*>(coeffs), N, rows, s);
     if (e == cudaSuccess) e = pdb::launch_wht_inplace(rows, N, 1ull << N, s);
     if (e == cudaSuccess)

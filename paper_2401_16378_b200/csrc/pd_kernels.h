@@ -51,6 +51,10 @@ cudaError_t launch_wht_from_matrix(const double2* G, unsigned N, uint64_t x0, ui
                                    cudaStream_t stream);
 
 // in-place unnormalised Walsh-Hadamard transform of x_count rows of 2^N (N <= 16)
+// recompose through the chunked inverse WHT passes (N in [11, 15]); scratch >= 4^N / 4 elements
+bool wht_inverse_ok(unsigned N);
+cudaError_t launch_wht_inverse(const double2* coeffs, unsigned N, double2* scratch, double2* G,
+                               cudaStream_t stream);
 cudaError_t launch_wht_inplace(double2* rows, unsigned N, uint64_t x_count, cudaStream_t stream);
 
 // recompose (decompose.cpp:221-250) on the device:

@@ -17,6 +17,7 @@
 #include <cstdlib>
 #include <mutex>
 
+#include <atomic>
 #include <cstdint>
 
 #include "pd_device.cuh"
@@ -359,6 +360,132 @@ __global__ void __launch_bounds__(kWhtThreads, 2)
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// Inverse transform for recompose (decompose.cpp:221-250), the forward passes run backwards.
+// Row x of the recomposed matrix, E_x[r] = G[r][r ^ x] = sum_z (-1)^{|r & z|} (-i)^{|x&z|} c_{x,z}
+// (pd_recompose.cu), is a Walsh-Hadamard transform over z split as z = (z_hi, z_lo), r = (r_hi,
+// r_lo): pass A (mirror of wht_hi_reg_kernel) reads the phased coefficients and butterflies the
+// high N-7 bits into E' [x][r_hi 128 + z_lo]; pass B (mirror of wht_gather_lo_reg_kernel)
+// butterflies the low 7 bits of 32 rows at once and writes the XOR-diagonal tiles of G.
+
+template <int HB>
+__global__ void __launch_bounds__(kWhtThreads, 2)
+    wht_inv_hi_kernel(const double2* __restrict__ coeffs, unsigned N, uint64_t x0,
+                      double2* __restrict__ eprime) {
+    static_assert(HB >= 4 && HB <= 8, "16 elements per thread in both rounds");
+    extern __shared__ __align__(16) double2 s2[];             // [2^HB][COLS]
+    constexpr int RB = HB - 4;
+    constexpr unsigned COLS = 1u << (12 - HB);
+    constexpr unsigned XPC_LOG = 9 - HB;
+    constexpr int PAIRS = 1 << (8 - HB);
+    const uint64_t dim = 1ull << N;
+    const uint64_t jb = blockIdx.x & 15;
+    const uint64_t xq = blockIdx.x >> 4;
+#pragma unroll
+    for (int q = 0; q < PAIRS; ++q) {
+        const unsigned p = threadIdx.x + q * kWhtThreads;
+        const unsigned col = p % COLS, hlo = p / COLS;
+        const uint64_t x = x0 + (xq << XPC_LOG) + (col >> 3);
+        double2 v[1 << RB];
+#pragma unroll
+        for (int h = 0; h < (1 << RB); ++h) {
+            const uint64_t z = (static_cast<uint64_t>((h << 4) | hlo) << kLoBits) | (jb << 3) | (col & 7);
+            const double2 c = __ldcs(&coeffs[tensor_number(x, z)]);
+            v[h] = apply_phase((3u * static_cast<unsigned>(__popcll(x & z))) & 3u, c.x, c.y, 1.0);
+        }
+#pragma unroll
+        for (int h = 1; h < (1 << RB); h <<= 1)
+#pragma unroll
+            for (int k = 0; k < (1 << RB); ++k)
+                if (!(k & h)) bfly(v[k], v[k + h]);
+#pragma unroll
+        for (int h = 0; h < (1 << RB); ++h) s2[((h << 4) | hlo) * COLS + col] = v[h];
+    }
+    __syncthreads();
+    const unsigned col = threadIdx.x % COLS, a = threadIdx.x / COLS;
+    double2 v[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = s2[((a << 4) | r) * COLS + col];
+#pragma unroll
+    for (int h = 1; h < 16; h <<= 1)
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            if (!(k & h)) bfly(v[k], v[k + h]);
+    double2* dst = eprime + ((xq << XPC_LOG) + (col >> 3)) * dim + (jb << 3) + (col & 7);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) dst[static_cast<uint64_t>((a << 4) | r) << kLoBits] = v[r];
+}
+
+// smem rows (rb 32 + x5) of 33 elements: the E' loads, the round over index bits 0-2 and the
+// transposed tile writes are all 4 wavefronts per warp
+__global__ void __launch_bounds__(kWhtThreads, 2)
+    wht_inv_lo_kernel(const double2* __restrict__ eprime, unsigned N, uint64_t x0,
+                      double2* __restrict__ G) {
+    extern __shared__ __align__(16) double2 sb[];              // [rb*32 + x5][33]
+    const uint64_t dim = 1ull << N;
+    const unsigned groups_log = N - kLoBits;
+    const uint64_t grp = blockIdx.x & ((1u << groups_log) - 1);   // r_hi: rows grp*128 ..
+    const uint64_t xb = blockIdx.x >> groups_log;
+    const uint64_t xh = (x0 >> 5) + xb;
+    // index bits 3-4 while loading 128 B lines of E' (and dropping them from L2)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const unsigned g = threadIdx.x + q * kWhtThreads, clo = g & 7, row = g >> 3;
+        const unsigned x5 = row >> 2, rb = row & 3;
+        const double2* src = eprime + ((xb << 5) + x5) * dim + (grp << kLoBits) + rb * 32 + clo;
+        double2 u[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) u[h] = __ldcs(src + h * 8);
+        if (clo == 0)
+#pragma unroll
+            for (int h = 0; h < 4; ++h)
+                asm volatile("discard.global.L2 [%0], 128;" ::"l"(src + h * 8) : "memory");
+        bfly(u[0], u[1]);
+        bfly(u[2], u[3]);
+        bfly(u[0], u[2]);
+        bfly(u[1], u[3]);
+#pragma unroll
+        for (int h = 0; h < 4; ++h) sb[(rb * 32 + x5) * kP1bRow + h * 8 + clo] = u[h];
+    }
+    __syncthreads();
+    // index bits 0-2
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        const unsigned g = threadIdx.x + q * kWhtThreads, row = g & 127, chi = g >> 7;
+        double2* r = sb + row * kP1bRow + chi * 8;
+        double2 u[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) u[e] = r[e];
+#pragma unroll
+        for (int h = 1; h < 8; h <<= 1)
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+                if (!(e & h)) bfly(u[e], u[e + h]);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) r[e] = u[e];
+    }
+    __syncthreads();
+    // index bits 5-6 in registers, then the 4 tiles (R = grp 4 + rb, C = R ^ x_h): element
+    // (tile row r, column c) is row r of X-mask x5 = r ^ c
+    const unsigned c = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const unsigned r = w + 8 * j, x5 = r ^ c;
+        double2 v[4];
+#pragma unroll
+        for (int rb = 0; rb < 4; ++rb) v[rb] = sb[(rb * 32 + x5) * kP1bRow + r];
+        bfly(v[0], v[1]);
+        bfly(v[2], v[3]);
+        bfly(v[0], v[2]);
+        bfly(v[1], v[3]);
+#pragma unroll
+        for (int rb = 0; rb < 4; ++rb) {
+            const uint64_t R = grp * 4 + rb, C = R ^ xh;
+            __stcs(&G[((R << 5) + r) * dim + (C << 5) + c], v[rb]);
+        }
+    }
+}
+
 }  // namespace
 
 // shared driver: rows pass, then (N > 12) the column pass; emit != 0 writes
@@ -547,6 +674,57 @@ cudaError_t launch_wht_from_matrix(const double2* G, unsigned N, uint64_t x0, ui
     for (uint64_t c = 0; e == cudaSuccess && c < x_count / S; ++c) {
         const int k = static_cast<int>(c % ns);  // slot k of D' belongs to stream k
         e = wht_two_pass(G, N, x0 + c * S, S, scratch + k * S * dim, map, true, p.side[k]);
+    }
+    for (int k = 0; e == cudaSuccess && k < ns; ++k) {
+        e = cudaEventRecord(p.join[k], p.side[k]);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, p.join[k], 0);
+    }
+    return e;
+}
+
+bool wht_inverse_ok(unsigned N) { return N >= 11 && N <= 15; }
+
+// recompose of the X-masks [0, 2^N) through the chunked L2-resident inverse passes (same
+// pipeline as launch_wht_from_matrix, data flowing the other way)
+cudaError_t launch_wht_inverse(const double2* coeffs, unsigned N, double2* scratch, double2* G,
+                               cudaStream_t stream) {
+    const uint64_t dim = 1ull << N;
+    const unsigned hb = N - kLoBits;
+    if (!wht_inverse_ok(N)) return cudaErrorNotSupported;
+    const uint64_t S0 = wht_chunk(N);
+    const uint64_t S = dim < 4 * S0 ? dim / 4 : S0;  // four chunks at least (S >= 32)
+    const size_t smem_a = sizeof(double2) * 4096, smem_b = kP1bSmem;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    static std::atomic<uint64_t> attr_set{0};
+    cudaError_t e = cudaSuccess;
+    if (!(attr_set.load() >> dev & 1)) {
+        for (auto k : {wht_inv_hi_kernel<4>, wht_inv_hi_kernel<5>, wht_inv_hi_kernel<6>, wht_inv_hi_kernel<7>,
+                       wht_inv_hi_kernel<8>})
+            if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_a);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(wht_inv_lo_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem_b));
+        if (e != cudaSuccess) return e;
+        attr_set.fetch_or(1ull << dev);
+    }
+    auto pass_a = hb == 4 ? wht_inv_hi_kernel<4> : hb == 5 ? wht_inv_hi_kernel<5> : hb == 6 ? wht_inv_hi_kernel<6>
+                : hb == 7 ? wht_inv_hi_kernel<7> : wht_inv_hi_kernel<8>;
+    WhtPipe& p = wht_pipe(dev);
+    if (!p.ok) return cudaErrorInitializationError;
+    std::lock_guard<std::mutex> lk(p.issue);
+    e = cudaEventRecord(p.fork, stream);
+    constexpr int ns = kWhtMaxStreams;
+    for (int k = 0; e == cudaSuccess && k < ns; ++k) e = cudaStreamWaitEvent(p.side[k], p.fork, 0);
+    for (uint64_t c = 0; e == cudaSuccess && c < dim / S; ++c) {
+        const int k = static_cast<int>(c % ns);
+        double2* slot = scratch + k * S * dim;
+        const unsigned grid_a = static_cast<unsigned>((S >> (9 - hb)) << 4);
+        pass_a<<<grid_a, kWhtThreads, smem_a, p.side[k]>>>(coeffs, N, c * S, slot);
+        const unsigned grid_b = static_cast<unsigned>((S >> 5) << (N - kLoBits));
+        wht_inv_lo_kernel<<<grid_b, kWhtThreads, smem_b, p.side[k]>>>(slot, N, c * S, G);
+        g_launches.fetch_add(2, std::memory_order_relaxed);
+        e = cudaGetLastError();
     }
     for (int k = 0; e == cudaSuccess && k < ns; ++k) {
         e = cudaEventRecord(p.join[k], p.side[k]);

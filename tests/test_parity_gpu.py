@@ -522,3 +522,26 @@ def test_sparse_batches_use_gathered_diagonals(pd, cuda, port, nq, count, n_x):
     got = pd.coefficients(g, ns)
     want = port.coeff_batch(g, ns)
     assert same_values(got, want)
+
+
+@pytest.mark.parametrize("nq", [11, 12, 13])
+def test_recompose_inverse_passes_round_trip(pd, cuda, port, nq):
+    """N >= 11 recomposes through the chunked inverse WHT passes: G -> c -> G within 1e-12 of
+    the largest element, and equal to the oracle's recompose on the same coefficients to the
+    same tolerance (both sum in different orders)."""
+    import torch
+    rng = np.random.default_rng(nq)
+    g = normal_matrix(rng, nq)
+    c = port.decompose(g) if nq == 11 else pd.decompose(g)  # the GPU path is pinned elsewhere
+    back = pd.recompose(c)
+    scale = np.max(np.abs(g))
+    assert np.max(np.abs(back - g)) <= 1e-12 * scale
+    if nq == 11:
+        assert np.max(np.abs(back - port.recompose(c))) <= 1e-12 * scale
+    # device form with the documented scratch size
+    cd = torch.from_numpy(c).to(cuda)
+    gd = torch.empty((2**nq, 2**nq), dtype=torch.complex128, device=cuda)
+    scr = torch.empty(4**nq, dtype=torch.complex128, device=cuda)
+    pd.device.recompose(nq, cd.data_ptr(), gd.data_ptr(), scr.data_ptr(), 0)
+    torch.cuda.synchronize()
+    assert np.max(np.abs(gd.cpu().numpy() - g)) <= 1e-12 * scale
