@@ -177,6 +177,10 @@ PD_EXPORT int pd_recompose_device(unsigned num_qubits, const double* coeffs, dou
 PD_EXPORT int pd_coeff_batch_device(unsigned num_qubits, const double* g, const uint64_t* ns, uint64_t count,
                           int slow, double* out, void* stream);
 
+/* random_matrix(N, seed) (bench.cpp:48-58) generated on the device and copied to g_out
+ * (2*4^N doubles); bit-identical to the reference's host generator. */
+PD_EXPORT int pd_random_matrix(pd_ctx* ctx, unsigned num_qubits, uint64_t seed, double* g_out);
+
 /* Device restatement of the reference's seeded generator random_matrix(N, seed)
  * (bench.cpp:16-58); bit-identical to it. */
 PD_EXPORT int pd_random_matrix_device(unsigned num_qubits, uint64_t seed, double* g, void* stream);

@@ -1,6 +1,7 @@
 // paulidecomp.cpp — the reference's C++ API (include/paulidecomp_b200/decompose.hpp) over the
 // C ABI of include/pd_api.h. Host logic only: validation, exception mapping, label algebra.
 // All arithmetic on matrices and coefficients happens in the CUDA kernels.
+#include "paulidecomp_b200/bench.hpp"
 #include "paulidecomp_b200/decompose.hpp"
 
 #include <bit>
@@ -196,6 +197,13 @@ Complex coeff_slow(const DenseMatrix& g, std::uint64_t n, MultCount& count) {
 
 Complex oracle_coeff_kron(const DenseMatrix& g, std::uint64_t n) {
     return oracle_coeff_view(g.data(), g.num_qubits(), n);
+}
+
+DenseMatrix random_matrix(unsigned num_qubits, std::uint64_t seed) {  // bench.cpp:48-58, on the GPU
+    DenseMatrix m(num_qubits);
+    Lease l = lease();
+    raise(pd_random_matrix(l.ctx, num_qubits, seed, as_doubles(m.data())));
+    return m;
 }
 
 PauliDecomposition decompose(const DenseMatrix& g, Path path) {

@@ -681,6 +681,18 @@ int decompose_multi(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pa
 
 }  // namespace
 
+int pd_random_matrix(pd_ctx* ctx, unsigned N, uint64_t seed, double* g_out) {
+    if (int rc = check_qubits(N)) return rc;
+    if (int rc = bind(ctx)) return rc;
+    if (!g_out) return fail(PD_EINVAL, "null buffer");
+    const size_t bytes = elems(N) * sizeof(double2);
+    if (int rc = ctx->ensure(&ctx->g, &ctx->g_bytes, bytes)) return rc;
+    if (int rc = pd_random_matrix_device(N, seed, static_cast<double*>(ctx->g), ctx->stream)) return rc;
+    PD_CUDA(cudaMemcpyAsync(g_out, ctx->g, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    PD_CUDA(cudaStreamSynchronize(ctx->stream));
+    return PD_OK;
+}
+
 int pd_recompose(pd_ctx* ctx, unsigned N, const double* coeffs, double* g_out) {
     if (int rc = check_qubits(N)) return rc;
     if (int rc = bind(ctx)) return rc;

@@ -174,3 +174,30 @@ def test_cli_subcommands(pd, ref, cuda, tmp_path):
     for args in (["decompose"], ["decompose", "--in", "/nonexistent"], ["frobnicate"],
                  ["decompose", "--in", src, "--eps", "-1"]):
         assert subprocess.run([CLI, *args], capture_output=True, timeout=60).returncode == 1, args
+
+
+@pytest.mark.gpu
+def test_cli_bench_csv(pd, port, cuda, tmp_path):
+    """`pdb200 bench` follows the reference's harness (main.cpp:110-128, bench.cpp:60-150): same
+    options, same generator seeds, same CSV schema, one mean row (rep -1) per (N, path) with
+    the sample stddev; the device paths must agree (the harness throws otherwise)."""
+    import csv as csvmod
+    out = str(tmp_path / "bench.csv")
+    r = subprocess.run([CLI, "bench", "--n-min", "1", "--n-max", "6", "--reps", "3", "--seed", "7",
+                        "--out", out], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    rows = list(csvmod.reader(open(out)))
+    assert rows[0] == ["N", "path", "threads", "rep", "seed", "seconds", "mult_count", "seconds_stddev"]
+    body = rows[1:]
+    assert len(body) == 6 * 3 * 4
+    for row in body:
+        nq, path, rep, seed = int(row[0]), row[1], int(row[3]), int(row[4])
+        assert path in ("gray", "wht", "naive")
+        if rep >= 0:
+            assert seed == port.matrix_seed(7, nq, rep) and row[7] == ""
+        else:
+            assert seed == 7 and float(row[7]) >= 0.0
+        if path == "gray":
+            assert int(row[6]) == 4**nq * (nq + 2 * 2**nq - 1)
+    for args in (["bench", "--n-max", "15"], ["bench", "--reps", "0"], ["bench", "--n-min", "3", "--n-max", "2"]):
+        assert subprocess.run([CLI, *args], capture_output=True, timeout=60).returncode == 1, args
