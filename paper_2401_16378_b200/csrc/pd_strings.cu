@@ -15,6 +15,7 @@
 // Gray order, with the exact factors ±1 folded into the sign bit, so the result equals K3 and
 // the reference's coeff_fast bit for bit (finite inputs); bucketing only changes which thread
 // computes a string, and results are written back at the string's own index.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <atomic>
@@ -131,25 +132,13 @@ constexpr int kSwStr = 1;
 
 constexpr int kSwWarps = 3;  // warps per bucket: a Poisson(64) bucket fits one round, one string per lane
 
-__global__ void __launch_bounds__(32 * kSwWarps)
-    strings_walk_kernel(const double2* __restrict__ G, unsigned N, const uint64_t* __restrict__ ns,
-                        const unsigned* __restrict__ order, const unsigned* __restrict__ off,
-                        double2* __restrict__ out, double scale) {
-    extern __shared__ __align__(16) double2 dx[];
-    const uint64_t x = blockIdx.x;
-    const unsigned begin = off[x], end = off[x + 1];
-    if (begin == end) return;
+// bucket x's strings over its staged diagonal (the caller stages dx and synchronises)
+__device__ __forceinline__ void walk_bucket(unsigned N, const uint64_t* __restrict__ ns,
+                                            const unsigned* __restrict__ order, unsigned begin,
+                                            unsigned end, uint64_t x, const double2* dx,
+                                            double2* __restrict__ out, double scale) {
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint64_t dim = 1ull << N;
-    for (uint64_t i = threadIdx.x; i < dim; i += 32 * kSwWarps) {
-        const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(dx + i));
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
-                     "l"(G + ((i ^ x) * dim + i))
-                     : "memory");
-    }
-    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
-    __syncthreads();
-    const uint64_t nblocks = dim >> kSwB;
+    const uint64_t nblocks = (1ull << N) >> kSwB;
     for (unsigned t0 = begin + warp * 32 * kSwStr; t0 < end; t0 += kSwWarps * 32 * kSwStr) {
         SwStrings<kSwStr> st;
         unsigned idx[kSwStr];
@@ -180,6 +169,85 @@ __global__ void __launch_bounds__(32 * kSwWarps)
             out[idx[j]] = apply_phase(ph, flip_hi(st.sr[j], st.sig[j]), flip_hi(st.si[j], st.sig[j]),
                                       scale);
         }
+    }
+}
+
+__device__ __forceinline__ void stage_diagonal(const double2* __restrict__ G, unsigned N, uint64_t x,
+                                               double2* dx) {
+    const uint64_t dim = 1ull << N;
+    for (uint64_t i = threadIdx.x; i < dim; i += blockDim.x) {
+        const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(dx + i));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
+                     "l"(G + ((i ^ x) * dim + i))
+                     : "memory");
+    }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(32 * kSwWarps)
+    strings_walk_kernel(const double2* __restrict__ G, unsigned N, const uint64_t* __restrict__ ns,
+                        const unsigned* __restrict__ order, const unsigned* __restrict__ off,
+                        double2* __restrict__ out, double scale) {
+    extern __shared__ __align__(16) double2 dx[];
+    const uint64_t x = blockIdx.x;
+    const unsigned begin = off[x], end = off[x + 1];
+    if (begin == end) return;
+    stage_diagonal(G, N, x, dx);
+    walk_bucket(N, ns, order, begin, end, x, dx, out, scale);
+}
+
+// The whole batch in one cooperative launch: zero the counts, count, scan + scatter, then
+// every CTA walks buckets x = blockIdx.x, + gridDim.x, ... (grid-wide syncs between phases).
+// One launch instead of a memset and three kernels: the batch call is launch bound.
+__global__ void __launch_bounds__(32 * kSwWarps)
+    strings_coop_kernel(const double2* __restrict__ G, unsigned N, const uint64_t* __restrict__ ns,
+                        uint64_t count, unsigned* __restrict__ cnt, unsigned* __restrict__ cur,
+                        unsigned* __restrict__ off, unsigned* __restrict__ order,
+                        double2* __restrict__ out, double scale) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ __align__(16) double2 dx[];
+    const unsigned nb = 1u << N;
+    for (uint64_t i = grid.thread_rank(); i < 2ull * nb; i += grid.size()) cnt[i] = 0;  // cnt, cur
+    grid.sync();
+    for (uint64_t k = grid.thread_rank(); k < count; k += grid.size()) atomicAdd(&cnt[xmask_of(ns[k])], 1u);
+    grid.sync();
+    {   // exclusive scan of the counts into shared memory (every CTA), then scatter
+        unsigned* start = reinterpret_cast<unsigned*>(dx);  // nb + 1 entries fit the D_x space
+        __shared__ unsigned part[32 * kSwWarps];
+        const unsigned nt = blockDim.x, per = (nb + nt - 1) / nt, b0 = threadIdx.x * per;
+        unsigned sum = 0;
+        for (unsigned j = 0; j < per && b0 + j < nb; ++j) sum += cnt[b0 + j];
+        part[threadIdx.x] = sum;
+        __syncthreads();
+        for (unsigned d = 1; d < nt; d <<= 1) {
+            const unsigned v = threadIdx.x >= d ? part[threadIdx.x - d] : 0u;
+            __syncthreads();
+            part[threadIdx.x] += v;
+            __syncthreads();
+        }
+        unsigned run = threadIdx.x ? part[threadIdx.x - 1] : 0u;
+        for (unsigned j = 0; j < per && b0 + j < nb; ++j) {
+            start[b0 + j] = run;
+            run += cnt[b0 + j];
+        }
+        if (threadIdx.x == nt - 1) start[nb] = part[nt - 1];
+        __syncthreads();
+        if (blockIdx.x == 0)
+            for (unsigned j = threadIdx.x; j <= nb; j += nt) off[j] = start[j];
+        for (uint64_t k = grid.thread_rank(); k < count; k += grid.size()) {
+            const uint64_t x = xmask_of(ns[k]);
+            order[start[x] + atomicAdd(&cur[x], 1u)] = static_cast<unsigned>(k);
+        }
+    }
+    grid.sync();
+    for (uint64_t x = blockIdx.x; x < nb; x += gridDim.x) {
+        const unsigned begin = off[x], end = off[x + 1];
+        if (begin == end) continue;
+        stage_diagonal(G, N, x, dx);
+        walk_bucket(N, ns, order, begin, end, x, dx, out, scale);
+        __syncthreads();  // dx is restaged for the next bucket
     }
 }
 
@@ -225,16 +293,38 @@ cudaError_t launch_strings_grouped(const double2* G, unsigned N, const uint64_t*
         }
         attr_set.fetch_or(1ull << dev);
     }
-    e = cudaMemsetAsync(cnt, 0, 2ull * nb * sizeof(unsigned), stream);
-    if (e == cudaSuccess) {
-        strings_count_kernel<<<static_cast<unsigned>((count + 255) / 256), 256, 0, stream>>>(ns, count, cnt);
-        strings_scatter_kernel<<<static_cast<unsigned>((count + kPrepThreads - 1) / kPrepThreads),
-                                 kPrepThreads, (nb + 1) * sizeof(unsigned), stream>>>(
-            ns, count, cnt, nb, cur, off, order);
-        strings_walk_kernel<<<nb, 32 * kSwWarps, smem, stream>>>(G, N, ns, order, off, out,
-                                                      1.0 / static_cast<double>(1ull << N));
-        g_launches.fetch_add(3, std::memory_order_relaxed);
-        e = cudaGetLastError();
+    static std::atomic<int> coop_grid[64][14] = {};  // co-resident CTAs per (device, N)
+    std::atomic<int>& cg_slot = coop_grid[dev & 63][N];
+    if (!cg_slot.load()) {
+        int per_sm = 0, sms = 0;
+        cudaFuncSetAttribute(strings_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(sizeof(double2) << 13));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, strings_coop_kernel, 32 * kSwWarps, smem);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaGetLastError();
+        cg_slot.store(per_sm * sms > 0 ? per_sm * sms : -1);
+    }
+    if (cg_slot.load() > 0) {
+        const double scale = 1.0 / static_cast<double>(1ull << N);
+        unsigned grid = static_cast<unsigned>(cg_slot.load());
+        if (grid > nb) grid = nb;
+        void* args[] = {const_cast<double2**>(&G), &N, const_cast<uint64_t**>(&ns), &count, &cnt, &cur,
+                        &off, &order, &out, const_cast<double*>(&scale)};
+        e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(strings_coop_kernel), grid, 32 * kSwWarps,
+                                        args, smem, stream);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+    } else {
+        e = cudaMemsetAsync(cnt, 0, 2ull * nb * sizeof(unsigned), stream);
+        if (e == cudaSuccess) {
+            strings_count_kernel<<<static_cast<unsigned>((count + 255) / 256), 256, 0, stream>>>(ns, count, cnt);
+            strings_scatter_kernel<<<static_cast<unsigned>((count + kPrepThreads - 1) / kPrepThreads),
+                                     kPrepThreads, (nb + 1) * sizeof(unsigned), stream>>>(
+                ns, count, cnt, nb, cur, off, order);
+            strings_walk_kernel<<<nb, 32 * kSwWarps, smem, stream>>>(G, N, ns, order, off, out,
+                                                                      1.0 / static_cast<double>(1ull << N));
+            g_launches.fetch_add(3, std::memory_order_relaxed);
+            e = cudaGetLastError();
+        }
     }
     cudaError_t f = cudaFreeAsync(scratch, stream);
     return e != cudaSuccess ? e : f;
