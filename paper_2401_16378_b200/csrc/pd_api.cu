@@ -22,6 +22,7 @@
 #include "pd_device.cuh"
 #include "pd_kernels.h"
 
+
 namespace {
 
 thread_local std::string t_error;
@@ -102,7 +103,7 @@ struct pd_ctx {
     cudaStream_t stream2 = nullptr;  // odd X-mask blocks (overlaps the previous block's tail)
     cudaStream_t d2h = nullptr;      // coefficient download, overlapped with later blocks
     cudaStream_t h2d = nullptr;      // column-segment upload + K1, overlapped with K2 segments
-    static constexpr int kBlocks = 16;  // 2^(download block bits)
+    static constexpr int kBlocks = 32;  // >= 2^(download block bits)
     static constexpr int kSegs = 4;     // walk segments
     cudaEvent_t gathered = nullptr;
     cudaEvent_t block_done[kBlocks] = {};
@@ -527,8 +528,8 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
     //    same ranges times the chunk length), each followed by K1 on those columns,
     //    while K2 runs the previous walk segment; K2 segments chain through raw partial sums,
     //    so the result is bit-identical to one launch. Otherwise G goes up in one copy.
-    //  * Download. The last K2 segment (or the whole WHT) runs in 16 X-mask blocks alternating
-    //    over two streams; block q's coefficients (16 runs of 4^(N-4), pd_run_offset) are copied
+    //  * Download. The last K2 segment (or the whole WHT) runs in 32 X-mask blocks alternating
+    //    over two streams; block q's coefficients (32 runs of 4^(N-5), pd_run_offset) are copied
     //    back while later blocks compute, so only the last block's D2H is exposed.
     double* dout = static_cast<double*>(ctx->out);
     double* diag = static_cast<double*>(ctx->scratch);
@@ -536,7 +537,7 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
     const bool gray = path == PD_PATH_GRAY;
     const unsigned nch = gray ? pdb::gray_xmask_chunks(N) : 1;
     const unsigned segs = nch >= 4 ? 4u : nch;
-    constexpr unsigned kBits = 4;  // 16 download blocks (measured: 8 -> 540, 16 -> 535 ms at N=14)
+    constexpr unsigned kBits = 5;  // 32 download blocks (N=14 e2e: 8 -> 540, 16 -> 520.4, 32 -> 518.1 ms)
     const uint64_t xc = dim >> kBits;
     const uint64_t run = 1ull << (2 * (N - kBits));
     double2* part = nullptr;
