@@ -104,7 +104,7 @@ struct pd_ctx {
     cudaStream_t d2h = nullptr;      // coefficient download, overlapped with later blocks
     cudaStream_t h2d = nullptr;      // column-segment upload + K1, overlapped with K2 segments
     static constexpr int kBlocks = 32;  // >= 2^(download block bits)
-    static constexpr int kSegs = 4;     // walk segments
+    static constexpr int kSegs = 5;     // walk segments
     cudaEvent_t gathered = nullptr;
     cudaEvent_t block_done[kBlocks] = {};
     cudaEvent_t cols_ready[kSegs] = {};
@@ -535,8 +535,11 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
     double* diag = static_cast<double*>(ctx->scratch);
     double* gdev = static_cast<double*>(ctx->g);
     const bool gray = path == PD_PATH_GRAY;
-    const unsigned nch = gray ? pdb::gray_xmask_chunks(N) : 1;
-    const unsigned segs = nch >= 4 ? 4u : nch;
+    // the host pipeline walks in chunks of 1024 columns (half K2's default) so that the first,
+    // exposed upload is 1/16 of G at N=14
+    constexpr unsigned kChunkLog = 10;
+    const unsigned nch = gray && pdb::gray_xmask_chunks(N) > 1 ? (1u << (N - kChunkLog)) : 1;
+    const unsigned segs = nch >= pd_ctx::kSegs ? pd_ctx::kSegs : nch;
     constexpr unsigned kBits = 5;  // 32 download blocks (N=14 e2e: 8 -> 540, 16 -> 520.4, 32 -> 518.1 ms)
     const uint64_t xc = dim >> kBits;
     const uint64_t run = 1ull << (2 * (N - kBits));
@@ -571,7 +574,7 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
             cudaError_t e = pdb::launch_gray_segment(reinterpret_cast<const double2*>(diag), N, 0,
                                                      dim, bnd[sg], bnd[sg + 1],
                                                      sg ? part : nullptr, part, 0, nullptr,
-                                                     PD_LAYOUT_GLOBAL, ctx->stream);
+                                                     PD_LAYOUT_GLOBAL, ctx->stream, kChunkLog);
             if (e != cudaSuccess) return cuda_fail(e, "gray segment launch");
         }
         c_last = bnd[nseg - 1];
@@ -590,7 +593,7 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
             cudaError_t e = pdb::launch_gray_segment(
                 reinterpret_cast<const double2*>(diag) + q * xc * dim, N, q * xc, xc, c_last, 0,
                 part ? part + q * xc * dim : nullptr, nullptr, 0,
-                reinterpret_cast<double2*>(dout), PD_LAYOUT_GLOBAL, s);
+                reinterpret_cast<double2*>(dout), PD_LAYOUT_GLOBAL, s, part ? kChunkLog : 0);
             rc = e == cudaSuccess ? PD_OK : cuda_fail(e, "gray block launch");
         } else {
             // WHT: each block gathers and transforms its own X-masks from G (fused two-pass)

@@ -61,7 +61,12 @@ static inline cudaError_t count_launch() {
 
 template <int K>
 static cudaError_t launch_gray(const K2Params& P0, cudaStream_t stream) {
-    const K2Geometry g = k2_geometry(P0.N, K, P0.x_count);
+    K2Geometry g = k2_geometry(P0.N, K, P0.x_count);
+    if (P0.ci_log && g.xc_log == 0 && P0.ci_log < g.ci_log && P0.ci_log > static_cast<unsigned>(K)) {
+        g.ci_log = P0.ci_log;  // shorter walk chunks (the host pipeline's first segments)
+        g.nchunks = 1u << (P0.N - g.ci_log);
+        g.smem_bytes = 2 * (sizeof(double2) << g.ci_log) + kK2BarBytes;
+    }
     static std::atomic<uint64_t> attr_set{0};  // per instantiation, one bit per device
     int dev = 0;
     cudaGetDevice(&dev);
@@ -108,8 +113,9 @@ static cudaError_t launch_gray(const K2Params& P0, cudaStream_t stream) {
 cudaError_t launch_gray_segment(const double2* diag, unsigned N, uint64_t x0, uint64_t x_count,
                                 unsigned c_begin, unsigned c_end, const double2* part_in,
                                 double2* part_out, unsigned run_bits, double2* out, int layout,
-                                cudaStream_t stream) {
+                                cudaStream_t stream, unsigned chunk_log) {
     K2Params P{};
+    P.ci_log = chunk_log;
     P.diag = diag;
     P.x0 = x0;
     P.x_count = x_count;

@@ -25,7 +25,7 @@ cudaError_t launch_diag_gather_cols(const double2* G, unsigned N, uint64_t x0, u
 cudaError_t launch_gray_segment(const double2* diag, unsigned N, uint64_t x0, uint64_t x_count,
                                 unsigned c_begin, unsigned c_end, const double2* part_in,
                                 double2* part_out, unsigned run_bits, double2* out, int layout,
-                                cudaStream_t stream);
+                                cudaStream_t stream, unsigned chunk_log = 0);
 unsigned gray_xmask_chunks(unsigned N);  // walk chunks per diagonal (1 for N < 12)
 
 // K2: Gray-code sums for the X-masks [x0, x0 + x_count); output layout as in pd_api.h
