@@ -49,8 +49,10 @@ from ._paulidecomp import (  # noqa: E402
     index_to_label,
     label_to_index,
     launch_count,
+    matrix_seed,
     oracle_coefficient,
     read_coefficients,
+    random_matrix,
     read_matrix,
     recompose,
     set_device,
@@ -76,8 +78,10 @@ __all__ = [
     "index_to_label",
     "label_to_index",
     "launch_count",
+    "matrix_seed",
     "oracle_coefficient",
     "read_coefficients",
+    "random_matrix",
     "read_matrix",
     "recompose",
     "set_device",

@@ -16,6 +16,7 @@
 #include <string>
 #include <vector>
 
+#include "paulidecomp_b200/bench.hpp"
 #include "paulidecomp_b200/decompose.hpp"
 #include "paulidecomp_b200/io.hpp"
 #include "pd_api.h"
@@ -228,6 +229,16 @@ PYBIND11_MODULE(_paulidecomp, m) {
           py::arg("path") = "gray",
           "Matrix file -> GPU decomposition -> threshold selection on the GPU -> coefficient CSV.");
 
+    m.def("matrix_seed", &matrix_seed, py::arg("seed"), py::arg("num_qubits"), py::arg("rep"),
+          "The reference benchmark's per-(N, rep) generator seed (bench.cpp:42-46).");
+    m.def("random_matrix", [](unsigned N, std::uint64_t seed) {
+        DenseMatrix g = random_matrix(N, seed);
+        const py::ssize_t dim = static_cast<py::ssize_t>(g.dim());
+        py::array_t<Complex> a({dim, dim});
+        std::memcpy(a.mutable_data(), g.data(), g.element_count() * sizeof(Complex));
+        return a;
+    }, py::arg("num_qubits"), py::arg("seed"),
+          "random_matrix(N, seed) of the reference benchmark (bench.cpp:48-58), generated on the GPU.");
     py::module_ d = m.def_submodule("device", "Stream-ordered entry points on device pointers");
     d.def("scratch_bytes", [](unsigned N, std::uint64_t x_count, const std::string& path) {
         return pd_scratch_bytes(N, x_count, path_of(path));

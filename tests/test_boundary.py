@@ -132,3 +132,15 @@ def test_product_package_never_touches_the_oracle():
                 text = open(os.path.join(dirpath, f), errors="ignore").read()
                 assert "import oracle" not in text and "from oracle" not in text, f
                 assert "libpd_oracle" not in text and "libpdref" not in text, f
+
+
+def test_matrix_seed_matches_reference(pd, port):
+    # bench.cpp:42-46, used by bench.py for the BASELINE configs[4] matrix
+    for seed, nq, rep in [(20260823, 14, 0), (1, 1, 0), (1, 5, 19), (2**63 + 5, 12, 7)]:
+        assert pd.matrix_seed(seed, nq, rep) == port.matrix_seed(seed, nq, rep)
+
+
+def test_bench_does_not_use_the_oracle_outside_its_cpu_legs():
+    src = open(os.path.join(ROOT, "bench.py")).read()
+    run_ours = src[src.index("def run_ours("):src.index("def side_configs(")]
+    assert "oracle" not in run_ours

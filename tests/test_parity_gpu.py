@@ -545,3 +545,9 @@ def test_recompose_inverse_passes_round_trip(pd, cuda, port, nq):
     pd.device.recompose(nq, cd.data_ptr(), gd.data_ptr(), scr.data_ptr(), 0)
     torch.cuda.synchronize()
     assert np.max(np.abs(gd.cpu().numpy() - g)) <= 1e-12 * scale
+
+
+def test_random_matrix_api_matches_reference_generator(pd, cuda, port):
+    for nq, seed in ((1, 3), (5, 77), (9, pd.matrix_seed(20260823, 9, 0))):
+        assert np.array_equal(pd.random_matrix(nq, seed).view(np.uint64),
+                              port.random_matrix(nq, seed).view(np.uint64))
