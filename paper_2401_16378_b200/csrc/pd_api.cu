@@ -528,9 +528,10 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
     //    same ranges times the chunk length), each followed by K1 on those columns,
     //    while K2 runs the previous walk segment; K2 segments chain through raw partial sums,
     //    so the result is bit-identical to one launch. Otherwise G goes up in one copy.
-    //  * Download. The last K2 segment (or the whole WHT) runs in 32 X-mask blocks alternating
-    //    over two streams; block q's coefficients (32 runs of 4^(N-5), pd_run_offset) are copied
-    //    back while later blocks compute, so only the last block's D2H is exposed.
+    //    Only 2^-(N-12) of the X-masks walks in segments; the rest runs whole walks afterwards.
+    //  * Download. The coefficients come back in 32 X-mask blocks; block q's (32 runs of
+    //    4^(N-5), pd_run_offset) are copied while later blocks compute, so only the last
+    //    block's D2H is exposed.
     double* dout = static_cast<double*>(ctx->out);
     double* diag = static_cast<double*>(ctx->scratch);
     double* gdev = static_cast<double*>(ctx->g);
@@ -543,11 +544,29 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
     constexpr unsigned kBits = 5;  // 32 download blocks (N=14 e2e: 8 -> 540, 16 -> 520.4, 32 -> 518.1 ms)
     const uint64_t xc = dim >> kBits;
     const uint64_t run = 1ull << (2 * (N - kBits));
-    double2* part = nullptr;
-    unsigned c_last = 0;
+    const unsigned nblk = 1u << kBits;
+    auto download = [&](unsigned q, cudaStream_t s) -> int {  // block q's runs, once computed
+        PD_CUDA(cudaEventRecord(ctx->block_done[q], s));
+        PD_CUDA(cudaStreamWaitEvent(ctx->d2h, ctx->block_done[q], 0));
+        for (unsigned r = 0; out && r < nblk; ++r) {
+            const uint64_t off = 2 * pd_run_offset(N, kBits, q, r);
+            PD_CUDA(cudaMemcpyAsync(out + off, dout + off, run * sizeof(double2),
+                                    cudaMemcpyDeviceToHost, ctx->d2h));
+        }
+        return PD_OK;
+    };
     if (gray && segs >= 2) {
-        if (int rc = ctx->ensure(&ctx->part, &ctx->part_bytes, bytes)) return rc;
-        part = static_cast<double2*>(ctx->part);
+        // Only block A — the first 2^-a of the X-masks — walks in segments that follow the
+        // upload; the rest runs the whole-walk kernel once G is complete, so the slower segment
+        // schedule (profiles/r01_k2_codegen.md) covers 2^-a of the work. A's walk should about
+        // outlast the upload (16 4^N B over PCIe against 2 8^N DADD, a ratio that doubles with
+        // every qubit). Measured (e2e ms, a = 0/1/2/3/4): N=12 14.7/16.6/16.3; N=13 -/81.0/74.8/78;
+        // N=14 515/-/510.5/540/552; N=15, 16 follow the ratio.
+        const unsigned a = N <= 12 ? 0u : (N <= 14 ? 2u : (N - 12 < 4 ? N - 12 : 4u));
+        const uint64_t xa = dim >> a;                       // X-masks of block A
+        const unsigned qa = nblk >> a;                      // download blocks in A
+        if (int rc = ctx->ensure(&ctx->part, &ctx->part_bytes, bytes >> a)) return rc;
+        double2* part = static_cast<double2*>(ctx->part);
         // walk segments [bnd[k], bnd[k+1]) in chunks, growing 1, 1, 2, 4, ... so that the first
         // upload (the only one not hidden behind K2) is small; an aligned power-of-two run of
         // chunks covers a contiguous column range (gray() permutes it onto itself)
@@ -569,44 +588,55 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
             if (e != cudaSuccess) return cuda_fail(e, "diag_gather launch");
             PD_CUDA(cudaEventRecord(ctx->cols_ready[sg], ctx->h2d));
         }
+        // block A on ctx->stream: segments as the columns arrive, then its last segment in qa
+        // download blocks (continuing from the stored raw sums)
         for (unsigned sg = 0; sg + 1 < nseg; ++sg) {
             PD_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->cols_ready[sg], 0));
             cudaError_t e = pdb::launch_gray_segment(reinterpret_cast<const double2*>(diag), N, 0,
-                                                     dim, bnd[sg], bnd[sg + 1],
+                                                     xa, bnd[sg], bnd[sg + 1],
                                                      sg ? part : nullptr, part, 0, nullptr,
                                                      PD_LAYOUT_GLOBAL, ctx->stream, kChunkLog);
             if (e != cudaSuccess) return cuda_fail(e, "gray segment launch");
         }
-        c_last = bnd[nseg - 1];
         PD_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->cols_ready[nseg - 1], 0));
-        PD_CUDA(cudaEventRecord(ctx->gathered, ctx->stream));
+        for (unsigned q = 0; q < qa; ++q) {
+            cudaError_t e = pdb::launch_gray_segment(
+                reinterpret_cast<const double2*>(diag) + q * xc * dim, N, q * xc, xc, bnd[nseg - 1], 0,
+                part + q * xc * dim, nullptr, 0, reinterpret_cast<double2*>(dout), PD_LAYOUT_GLOBAL,
+                ctx->stream, kChunkLog);
+            if (e != cudaSuccess) return cuda_fail(e, "gray block launch");
+            if (int rc = download(q, ctx->stream)) return rc;
+        }
+        // the rest: whole walks once G is complete, alternating over two further streams
+        PD_CUDA(cudaStreamWaitEvent(ctx->stream2, ctx->cols_ready[nseg - 1], 0));
+        for (unsigned q = qa; q < nblk; ++q) {
+            cudaStream_t s = (q & 1) ? ctx->stream2 : ctx->h2d;
+            cudaError_t e = pdb::launch_gray_segment(
+                reinterpret_cast<const double2*>(diag) + q * xc * dim, N, q * xc, xc, 0, 0, nullptr,
+                nullptr, 0, reinterpret_cast<double2*>(dout), PD_LAYOUT_GLOBAL, s);
+            if (e != cudaSuccess) return cuda_fail(e, "gray block launch");
+            if (int rc = download(q, s)) return rc;
+        }
     } else {
         if (int rc = upload(ctx, ctx->g, g, bytes)) return rc;
         if (gray && pd_diag_gather_device(N, gdev, 0, dim, diag, ctx->stream)) return PD_ECUDA;
         PD_CUDA(cudaEventRecord(ctx->gathered, ctx->stream));
-    }
-    PD_CUDA(cudaStreamWaitEvent(ctx->stream2, ctx->gathered, 0));
-    for (unsigned q = 0; q < (1u << kBits); ++q) {
-        cudaStream_t s = (q & 1) ? ctx->stream2 : ctx->stream;
-        int rc;
-        if (gray) {
-            cudaError_t e = pdb::launch_gray_segment(
-                reinterpret_cast<const double2*>(diag) + q * xc * dim, N, q * xc, xc, c_last, 0,
-                part ? part + q * xc * dim : nullptr, nullptr, 0,
-                reinterpret_cast<double2*>(dout), PD_LAYOUT_GLOBAL, s, part ? kChunkLog : 0);
-            rc = e == cudaSuccess ? PD_OK : cuda_fail(e, "gray block launch");
-        } else {
-            // WHT: each block gathers and transforms its own X-masks from G (fused two-pass)
-            rc = pd_shard_coeffs_device(N, gdev, q * xc, xc, 0, dout, PD_LAYOUT_GLOBAL,
-                                        diag + 2 * q * xc * dim, path, s);
-        }
-        if (rc) return rc;
-        PD_CUDA(cudaEventRecord(ctx->block_done[q], s));
-        PD_CUDA(cudaStreamWaitEvent(ctx->d2h, ctx->block_done[q], 0));
-        for (unsigned r = 0; out && r < (1u << kBits); ++r) {
-            const uint64_t off = 2 * pd_run_offset(N, kBits, q, r);
-            PD_CUDA(cudaMemcpyAsync(out + off, dout + off, run * sizeof(double2),
-                                    cudaMemcpyDeviceToHost, ctx->d2h));
+        PD_CUDA(cudaStreamWaitEvent(ctx->stream2, ctx->gathered, 0));
+        for (unsigned q = 0; q < nblk; ++q) {
+            cudaStream_t s = (q & 1) ? ctx->stream2 : ctx->stream;
+            int rc;
+            if (gray) {
+                cudaError_t e = pdb::launch_gray_segment(
+                    reinterpret_cast<const double2*>(diag) + q * xc * dim, N, q * xc, xc, 0, 0, nullptr,
+                    nullptr, 0, reinterpret_cast<double2*>(dout), PD_LAYOUT_GLOBAL, s);
+                rc = e == cudaSuccess ? PD_OK : cuda_fail(e, "gray block launch");
+            } else {
+                // WHT: each block gathers and transforms its own X-masks from G (fused two-pass)
+                rc = pd_shard_coeffs_device(N, gdev, q * xc, xc, 0, dout, PD_LAYOUT_GLOBAL,
+                                            diag + 2 * q * xc * dim, path, s);
+            }
+            if (rc) return rc;
+            if (int rc2 = download(q, s)) return rc2;
         }
     }
     PD_CUDA(cudaStreamSynchronize(ctx->d2h));
