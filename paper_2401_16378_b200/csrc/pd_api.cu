@@ -510,7 +510,25 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
     if (int rc = ctx->ensure(&ctx->g, &ctx->g_bytes, bytes)) return rc;
     if (int rc = ctx->ensure(&ctx->out, &ctx->out_bytes, bytes)) return rc;
     const uint64_t sb = pd_scratch_bytes(N, 1ull << N, path);
-    if (sb && (ctx->ensure(&ctx->scratch, &ctx->scratch_bytes, sb) != PD_OK)) return PD_ENOMEM;
+    if (sb && ctx->scratch_bytes < sb) {
+        // G and the coefficients fit but not a full set of diagonals (N = 16 on one B200:
+        // 3 x 64 GiB): upload, decompose in X-mask blocks sized to what is free, download
+        if (ctx->ensure(&ctx->scratch, &ctx->scratch_bytes, sb) != PD_OK) {
+            size_t free_b = 0, total_b = 0;
+            cudaGetLastError();
+            PD_CUDA(cudaMemGetInfo(&free_b, &total_b));
+            const size_t want = free_b > (1ull << 30) ? free_b - (1ull << 30) : 0;  // 1 GiB margin
+            if (int rc = ctx->ensure(&ctx->scratch, &ctx->scratch_bytes, want)) return rc;
+            if (int rc = upload(ctx, ctx->g, g, bytes)) return rc;
+            if (int rc = pd_decompose_device_blocked(N, static_cast<const double*>(ctx->g),
+                                                     static_cast<double*>(ctx->out), ctx->scratch,
+                                                     ctx->scratch_bytes, path, ctx->stream))
+                return rc;
+            if (out) PD_CUDA(cudaMemcpyAsync(out, ctx->out, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+            PD_CUDA(cudaStreamSynchronize(ctx->stream));
+            return PD_OK;
+        }
+    }
     const uint64_t dim = 1ull << N;
     if (path == PD_PATH_NAIVE || N < 10) {
         if (int rc = upload(ctx, ctx->g, g, bytes)) return rc;

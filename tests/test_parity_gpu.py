@@ -8,7 +8,7 @@ an exact zero may differ). The WHT path is held to the tolerance.
 import numpy as np
 import pytest
 
-from conftest import normal_matrix, same_values
+from conftest import ROOT, normal_matrix, same_values
 from oracle import oracle as O
 
 pytestmark = pytest.mark.gpu
@@ -551,3 +551,29 @@ def test_random_matrix_api_matches_reference_generator(pd, cuda, port):
     for nq, seed in ((1, 3), (5, 77), (9, pd.matrix_seed(20260823, 9, 0))):
         assert np.array_equal(pd.random_matrix(nq, seed).view(np.uint64),
                               port.random_matrix(nq, seed).view(np.uint64))
+
+
+def test_host_path_falls_back_to_blocked_scratch_when_memory_is_short(cuda):
+    """With G and the coefficients resident but no room for every diagonal (N=16 on one B200),
+    pd_decompose uploads, decomposes in X-mask blocks sized to the free memory and downloads.
+    Simulated at N=14 in a fresh process by filling all but ~10 GiB of the device first; the
+    result must equal the normal pipelined path bit for bit."""
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+import paper_2401_16378_b200 as pd
+nq = 14
+g = pd.random_matrix(nq, 4141)
+free, _ = torch.cuda.mem_get_info()
+filler = torch.empty(free - (10 << 30), dtype=torch.uint8, device="cuda")
+a = pd.decompose(g)
+del filler
+torch.cuda.empty_cache()
+b = pd.decompose(g)
+assert np.array_equal(a, b)
+print("ok")
+''' % ROOT
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
