@@ -185,9 +185,12 @@ class ShardedDecomposer:
             return G, out
         msg = [None]
         if p.rank == 0:
-            key = (G.data_ptr(), out.data_ptr())
+            # exported on every call (cheap): the handles identify the allocations, so a buffer
+            # freed and reallocated at the same address is still noticed by the peers
+            hg, ho = self.mapper.export(G), self.mapper.export(out)
+            key = (G.data_ptr(), out.data_ptr(), hg, ho)
             if key != self._peer_key:
-                self._peer_msg = (key, self.mapper.export(G), self.mapper.export(out))
+                self._peer_msg = (key, hg, ho)
                 self._peer_key = key
             msg = [self._peer_msg]
         dist.broadcast_object_list(msg, src=0, group=self.group)
