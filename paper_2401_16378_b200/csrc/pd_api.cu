@@ -260,6 +260,7 @@ uint64_t pd_run_offset(unsigned N, unsigned run_bits, uint64_t shard, uint64_t r
 int pd_diag_gather_device(unsigned N, const double* g, uint64_t x0, uint64_t x_count,
                           double* diag, void* stream) {
     if (int rc = check_qubits(N)) return rc;
+    if (!g || !diag) return fail(PD_EINVAL, "null buffer");
     if (int rc = check_device()) return rc;
     if (x_count == 0 || (x_count & (x_count - 1)) || x0 % x_count || x0 + x_count > (1ull << N))
         return fail(PD_EINVAL, "X-mask range must be an aligned power-of-two block inside [0, 2^N)");
@@ -335,6 +336,7 @@ int pd_shard_coeffs_device(unsigned N, const double* g, uint64_t x0, uint64_t x_
 int pd_decompose_device(unsigned N, const double* g, double* out, void* scratch, pd_path path,
                         void* stream) {
     if (int rc = check_qubits(N)) return rc;
+    if (!g || !out) return fail(PD_EINVAL, "null buffer");
     if (int rc = check_device()) return rc;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (path == PD_PATH_NAIVE) {
@@ -372,6 +374,7 @@ int pd_decompose_device_blocked(unsigned N, const double* g, double* out, void* 
 int pd_coeff_batch_device(unsigned N, const double* g, const uint64_t* ns, uint64_t count, int slow,
                           double* out, void* stream) {
     if (int rc = check_qubits(N)) return rc;
+    if (count && (!g || !ns || !out)) return fail(PD_EINVAL, "null buffer");
     if (int rc = check_device()) return rc;
     cudaError_t e = pdb::launch_walk(reinterpret_cast<const double2*>(g), N, ns, count, slow != 0,
                                      reinterpret_cast<double2*>(out),
@@ -404,6 +407,7 @@ int pd_recompose_device(unsigned N, const double* coeffs, double* g_out, void* s
 
 int pd_random_matrix_device(unsigned N, uint64_t seed, double* g, void* stream) {
     if (int rc = check_qubits(N)) return rc;
+    if (!g) return fail(PD_EINVAL, "null buffer");
     if (int rc = check_device()) return rc;
     cudaError_t e = pdb::launch_random_matrix(N, seed, reinterpret_cast<double2*>(g),
                                               static_cast<cudaStream_t>(stream));
@@ -765,6 +769,7 @@ int pd_recompose(pd_ctx* ctx, unsigned N, const double* coeffs, double* g_out) {
 int pd_coeff_batch(pd_ctx* ctx, unsigned N, const double* g, const uint64_t* ns, uint64_t count,
                    double* out) {
     if (int rc = check_qubits(N)) return rc;
+    if (count && (!g || !ns || !out)) return fail(PD_EINVAL, "null buffer");
     for (uint64_t k = 0; k < count; ++k)
         if (int rc = check_index(N, ns[k])) return rc;
     if (int rc = bind(ctx)) return rc;
@@ -831,6 +836,7 @@ int pd_coeff_batch(pd_ctx* ctx, unsigned N, const double* g, const uint64_t* ns,
 
 int pd_coeff(pd_ctx* ctx, unsigned N, const double* g, uint64_t n, int slow, double* out) {
     if (int rc = check_qubits(N)) return rc;
+    if (!g || !out) return fail(PD_EINVAL, "null buffer");
     if (int rc = check_index(N, n)) return rc;
     if (int rc = bind(ctx)) return rc;
     // one string reads one XOR-diagonal: gather its 2^N elements on the host (16 KiB at N=10,
@@ -867,6 +873,7 @@ int pd_coeff(pd_ctx* ctx, unsigned N, const double* g, uint64_t n, int slow, dou
 
 int pd_oracle_coeff(pd_ctx* ctx, unsigned N, const double* g, uint64_t n, double* out) {
     if (int rc = check_qubits(N)) return rc;
+    if (!g || !out) return fail(PD_EINVAL, "null buffer");
     if (int rc = check_index(N, n)) return rc;
     if (N > kOracleMaxQubits)
         return fail(PD_EINVAL, "reference path is capped at %u qubits", kOracleMaxQubits);

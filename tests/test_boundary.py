@@ -144,3 +144,22 @@ def test_bench_does_not_use_the_oracle_outside_its_cpu_legs():
     src = open(os.path.join(ROOT, "bench.py")).read()
     run_ours = src[src.index("def run_ours("):src.index("def side_configs(")]
     assert "oracle" not in run_ours
+
+
+def test_c_abi_rejects_null_buffers_before_device_work(pd):
+    lib = ctypes.CDLL(pd.LIBRARY_PATH)
+    lib.pd_last_error.restype = ctypes.c_char_p
+    vp = ctypes.c_void_p
+    lib.pd_coeff_batch.argtypes = [vp, ctypes.c_uint, vp, vp, ctypes.c_uint64, vp]
+    assert lib.pd_coeff_batch(None, 4, None, None, 3, None) == -1
+    lib.pd_coeff_batch_device.argtypes = [ctypes.c_uint, vp, vp, ctypes.c_uint64, ctypes.c_int, vp, vp]
+    assert lib.pd_coeff_batch_device(4, None, None, 3, 0, None, None) == -1
+    lib.pd_decompose_device.argtypes = [ctypes.c_uint, vp, vp, vp, ctypes.c_int, vp]
+    assert lib.pd_decompose_device(4, None, None, None, 0, None) == -1
+    lib.pd_coeff.argtypes = [vp, ctypes.c_uint, vp, ctypes.c_uint64, ctypes.c_int, vp]
+    assert lib.pd_coeff(None, 4, None, 0, 0, None) == -1
+    assert b"null" in lib.pd_last_error()
+    lib.pd_ctx_create_multi.argtypes = [vp, ctypes.c_int, vp]
+    out = vp()
+    devs = (ctypes.c_int * 3)(0, 0, 0)
+    assert lib.pd_ctx_create_multi(devs, 3, ctypes.byref(out)) == -1   # not a power of two
