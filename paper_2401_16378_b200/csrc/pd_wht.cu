@@ -393,39 +393,57 @@ __global__ void __launch_bounds__(kWhtThreads, 2)
     const uint64_t dim = 1ull << N;
     const uint64_t jb = blockIdx.x & 15;
     const uint64_t xq = blockIdx.x >> 4;
+    // all PAIRS x 2^RB scattered coefficient reads are issued before any is used (16 in flight
+    // per thread), then phased and butterflied; tensor numbers from a per-thread part and
+    // compile-time spreads (wht_hi_reg_kernel)
+    constexpr unsigned kHiShift = kLoBits + 4;
+    double2 v[PAIRS][1 << RB];
+    unsigned ph[PAIRS][1 << RB];
 #pragma unroll
     for (int q = 0; q < PAIRS; ++q) {
         const unsigned p = threadIdx.x + q * kWhtThreads;
         const unsigned col = p % COLS, hlo = p / COLS;
         const uint64_t x = x0 + (xq << XPC_LOG) + (col >> 3);
-        double2 v[1 << RB];
+        const uint64_t zl = (static_cast<uint64_t>(hlo) << kLoBits) | (jb << 3) | (col & 7);
+        const uint64_t xh = x >> kHiShift << kHiShift;
+        const uint64_t nl = spread_bits((x ^ zl) & ((1ull << kHiShift) - 1)) | (spread_bits(zl) << 1);
+        const uint64_t sxh = spread_bits(xh);
+        const unsigned pl = static_cast<unsigned>(__popcll(x & zl));
 #pragma unroll
         for (int h = 0; h < (1 << RB); ++h) {
-            const uint64_t z = (static_cast<uint64_t>((h << 4) | hlo) << kLoBits) | (jb << 3) | (col & 7);
-            const double2 c = __ldcs(&coeffs[tensor_number(x, z)]);
-            v[h] = apply_phase((3u * static_cast<unsigned>(__popcll(x & z))) & 3u, c.x, c.y, 1.0);
+            const uint64_t zh = static_cast<uint64_t>(h) << kHiShift;
+            const uint64_t szh = spread_bits(zh);  // constant
+            v[q][h] = __ldcs(&coeffs[nl | (sxh ^ szh) | (szh << 1)]);
+            ph[q][h] = (3u * (pl + static_cast<unsigned>(__popcll(xh & zh)))) & 3u;
         }
+    }
+#pragma unroll
+    for (int q = 0; q < PAIRS; ++q) {
+        const unsigned p = threadIdx.x + q * kWhtThreads;
+        const unsigned col = p % COLS, hlo = p / COLS;
+#pragma unroll
+        for (int h = 0; h < (1 << RB); ++h) v[q][h] = apply_phase(ph[q][h], v[q][h].x, v[q][h].y, 1.0);
 #pragma unroll
         for (int h = 1; h < (1 << RB); h <<= 1)
 #pragma unroll
             for (int k = 0; k < (1 << RB); ++k)
-                if (!(k & h)) bfly(v[k], v[k + h]);
+                if (!(k & h)) bfly(v[q][k], v[q][k + h]);
 #pragma unroll
-        for (int h = 0; h < (1 << RB); ++h) s2[((h << 4) | hlo) * COLS + col] = v[h];
+        for (int h = 0; h < (1 << RB); ++h) s2[((h << 4) | hlo) * COLS + col] = v[q][h];
     }
     __syncthreads();
     const unsigned col = threadIdx.x % COLS, a = threadIdx.x / COLS;
-    double2 v[16];
+    double2 w[16];
 #pragma unroll
-    for (int r = 0; r < 16; ++r) v[r] = s2[((a << 4) | r) * COLS + col];
+    for (int r = 0; r < 16; ++r) w[r] = s2[((a << 4) | r) * COLS + col];
 #pragma unroll
     for (int h = 1; h < 16; h <<= 1)
 #pragma unroll
         for (int k = 0; k < 16; ++k)
-            if (!(k & h)) bfly(v[k], v[k + h]);
+            if (!(k & h)) bfly(w[k], w[k + h]);
     double2* dst = eprime + ((xq << XPC_LOG) + (col >> 3)) * dim + (jb << 3) + (col & 7);
 #pragma unroll
-    for (int r = 0; r < 16; ++r) dst[static_cast<uint64_t>((a << 4) | r) << kLoBits] = v[r];
+    for (int r = 0; r < 16; ++r) dst[static_cast<uint64_t>((a << 4) | r) << kLoBits] = w[r];
 }
 
 // smem rows (rb 32 + x5) of 33 elements: the E' loads, the round over index bits 0-2 and the
