@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -104,7 +105,7 @@ struct pd_ctx {
     cudaStream_t d2h = nullptr;      // coefficient download, overlapped with later blocks
     cudaStream_t h2d = nullptr;      // column-segment upload + K1, overlapped with K2 segments
     static constexpr int kBlocks = 32;  // >= 2^(download block bits)
-    static constexpr int kSegs = 5;     // walk segments
+    static constexpr int kSegs = 40;    // walk segments
     cudaEvent_t gathered = nullptr;
     cudaEvent_t block_done[kBlocks] = {};
     cudaEvent_t cols_ready[kSegs] = {};
@@ -530,6 +531,10 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
                 return rc;
             if (out) PD_CUDA(cudaMemcpyAsync(out, ctx->out, bytes, cudaMemcpyDeviceToHost, ctx->stream));
             PD_CUDA(cudaStreamSynchronize(ctx->stream));
+            // the scratch took all but 1 GiB of the device: give it back rather than keep it cached
+            PD_CUDA(cudaFree(ctx->scratch));
+            ctx->scratch = nullptr;
+            ctx->scratch_bytes = 0;
             return PD_OK;
         }
     }
@@ -560,7 +565,7 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
     const bool gray = path == PD_PATH_GRAY;
     // the host pipeline walks in chunks of 1024 columns (half K2's default) so that the first,
     // exposed upload is 1/16 of G at N=14
-    constexpr unsigned kChunkLog = 10;
+    constexpr unsigned kChunkLog = 10;  // 9 and 11 measured 500.5 and 508 ms (N=14 e2e)
     const unsigned nch = gray && pdb::gray_xmask_chunks(N) > 1 ? (1u << (N - kChunkLog)) : 1;
     const unsigned segs = nch >= pd_ctx::kSegs ? pd_ctx::kSegs : nch;
     constexpr unsigned kBits = 5;  // 32 download blocks (N=14 e2e: 8 -> 540, 16 -> 520.4, 32 -> 518.1 ms)
@@ -589,18 +594,30 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
         const unsigned qa = nblk >> a;                      // download blocks in A
         if (int rc = ctx->ensure(&ctx->part, &ctx->part_bytes, bytes >> a)) return rc;
         double2* part = static_cast<double2*>(ctx->part);
-        // walk segments [bnd[k], bnd[k+1]) in chunks, growing 1, 1, 2, 4, ... so that the first
-        // upload (the only one not hidden behind K2) is small; an aligned power-of-two run of
-        // chunks covers a contiguous column range (gray() permutes it onto itself)
+        // walk segments [bnd[k], bnd[k+1]) in chunks: `ones` single chunks (the first upload,
+        // the only one not hidden behind K2, is one chunk), then aligned runs of `runlen` chunks,
+        // so that block A's walk follows the upload instead of idling until a long segment's
+        // columns have arrived. N=14 e2e: doubling segments 1, 1, 2, 4, 8 510-515 ms; 4 x 1 then
+        // runs of 2: 500.5 ms (2 x 1 then 2: 502.9; 4 x 1 then 1: 502; then 4: 504; a = 1: 548;
+        // a = 3: 515)
+        constexpr unsigned ones = 4, runlen = 2;
         unsigned bnd[pd_ctx::kSegs + 1];
         unsigned nb = 0;
         bnd[nb++] = 0;
-        for (unsigned c = 1; nb < segs && c < nch; c <<= 1) bnd[nb++] = c;
-        bnd[nb] = nch;
-        const unsigned nseg = nb;
+        for (unsigned c = 0; c < nch;) {
+            unsigned L = nb - 1 < ones ? 1u : runlen;
+            while (L > 1 && (c % L || c + L > nch)) L >>= 1;
+            if (nb == pd_ctx::kSegs) return fail(PD_EINVAL, "walk segment plan too long");
+            c += L;
+            bnd[nb++] = c;
+        }
+        const unsigned nseg = nb - 1;
         const uint64_t C = dim / nch;  // columns per walk chunk
         for (unsigned sg = 0; sg < nseg; ++sg) {
-            const uint64_t col0 = bnd[sg] * C, W = (bnd[sg + 1] - bnd[sg]) * C;
+            // an aligned run of L chunks visits the aligned run of L column chunks holding gray(b)
+            const uint64_t L = bnd[sg + 1] - bnd[sg];
+            const uint64_t gb = bnd[sg] ^ (bnd[sg] >> 1);
+            const uint64_t col0 = (gb & ~(L - 1)) * C, W = L * C;
             PD_CUDA(cudaMemcpy2DAsync(gdev + 2 * col0, dim * sizeof(double2), g + 2 * col0,
                                       dim * sizeof(double2), W * sizeof(double2), dim,
                                       cudaMemcpyHostToDevice, ctx->h2d));
