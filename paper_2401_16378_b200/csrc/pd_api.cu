@@ -103,12 +103,15 @@ struct pd_ctx {
     cudaStream_t stream = nullptr;   // H2D, K1, even X-mask blocks
     cudaStream_t stream2 = nullptr;  // odd X-mask blocks (overlaps the previous block's tail)
     cudaStream_t d2h = nullptr;      // coefficient download, overlapped with later blocks
-    cudaStream_t h2d = nullptr;      // column-segment upload + K1, overlapped with K2 segments
+    cudaStream_t h2d = nullptr;      // column-segment upload, overlapped with K2 segments
+    cudaStream_t gather = nullptr;   // K1 on each uploaded segment (high priority: its CTAs are
+                                     // dispatched ahead of the K2 walk's pending ones)
     static constexpr int kBlocks = 32;  // >= 2^(download block bits)
     static constexpr int kSegs = 40;    // walk segments
     cudaEvent_t gathered = nullptr;
     cudaEvent_t block_done[kBlocks] = {};
     cudaEvent_t cols_ready[kSegs] = {};
+    cudaEvent_t copied[kSegs] = {};
     cudaEvent_t seg_done = nullptr;
     void* part = nullptr;            // raw partial sums between walk segments
     size_t part_bytes = 0;
@@ -183,12 +186,17 @@ int pd_ctx_create(int device, pd_ctx** out) {
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking);
+    int prio_lo = 0, prio_hi = 0;
+    if (e == cudaSuccess) e = cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+    if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&ctx->gather, cudaStreamNonBlocking, prio_hi);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->gathered, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->seg_done, cudaEventDisableTiming);
     for (int b = 0; e == cudaSuccess && b < pd_ctx::kBlocks; ++b)
         e = cudaEventCreateWithFlags(&ctx->block_done[b], cudaEventDisableTiming);
     for (int b = 0; e == cudaSuccess && b < pd_ctx::kSegs; ++b)
         e = cudaEventCreateWithFlags(&ctx->cols_ready[b], cudaEventDisableTiming);
+    for (int b = 0; e == cudaSuccess && b < pd_ctx::kSegs; ++b)
+        e = cudaEventCreateWithFlags(&ctx->copied[b], cudaEventDisableTiming);
     if (e != cudaSuccess) {
         pd_ctx_destroy(ctx);
         return cuda_fail(e, "cudaStreamCreate");
@@ -223,7 +231,7 @@ int pd_ctx_destroy(pd_ctx* ctx) {
     if (ctx->stage) cudaFreeHost(ctx->stage);
     ctx->stage = nullptr;
     cudaSetDevice(ctx->device);
-    for (cudaStream_t s : {ctx->stream, ctx->stream2, ctx->d2h, ctx->h2d})
+    for (cudaStream_t s : {ctx->stream, ctx->stream2, ctx->d2h, ctx->h2d, ctx->gather})
         if (s) cudaStreamSynchronize(s);
     for (void* p : {ctx->g, ctx->out, ctx->scratch, ctx->ns, ctx->part, ctx->sel_tiles, ctx->sel_idx,
                     ctx->sel_val})
@@ -234,7 +242,9 @@ int pd_ctx_destroy(pd_ctx* ctx) {
         if (ev) cudaEventDestroy(ev);
     for (cudaEvent_t ev : ctx->cols_ready)
         if (ev) cudaEventDestroy(ev);
-    for (cudaStream_t s : {ctx->stream, ctx->stream2, ctx->d2h, ctx->h2d})
+    for (cudaEvent_t ev : ctx->copied)
+        if (ev) cudaEventDestroy(ev);
+    for (cudaStream_t s : {ctx->stream, ctx->stream2, ctx->d2h, ctx->h2d, ctx->gather})
         if (s) cudaStreamDestroy(s);
     delete ctx;
     return PD_OK;
@@ -555,7 +565,6 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
     //    same ranges times the chunk length), each followed by K1 on those columns,
     //    while K2 runs the previous walk segment; K2 segments chain through raw partial sums,
     //    so the result is bit-identical to one launch. Otherwise G goes up in one copy.
-    //    Only 2^-(N-12) of the X-masks walks in segments; the rest runs whole walks afterwards.
     //  * Download. The coefficients come back in 32 X-mask blocks; block q's (32 runs of
     //    4^(N-5), pd_run_offset) are copied while later blocks compute, so only the last
     //    block's D2H is exposed.
@@ -582,35 +591,39 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
         }
         return PD_OK;
     };
-    if (gray && segs >= 2) {
-        // Only block A — the first 2^-a of the X-masks — walks in segments that follow the
-        // upload; the rest runs the whole-walk kernel once G is complete, so the slower segment
-        // schedule (profiles/r01_k2_codegen.md) covers 2^-a of the work. A's walk should about
-        // outlast the upload (16 4^N B over PCIe against 2 8^N DADD, a ratio that doubles with
-        // every qubit). Measured (e2e ms, a = 0/1/2/3/4): N=12 14.7/16.6/16.3; N=13 -/81.0/74.8/78;
-        // N=14 515/-/510.5/540/552; N=15, 16 follow the ratio.
-        const unsigned a = N <= 12 ? 0u : (N <= 14 ? 2u : (N - 12 < 4 ? N - 12 : 4u));
-        const uint64_t xa = dim >> a;                       // X-masks of block A
-        const unsigned qa = nblk >> a;                      // download blocks in A
-        if (int rc = ctx->ensure(&ctx->part, &ctx->part_bytes, bytes >> a)) return rc;
+    // the walk segments keep raw partial sums of every coefficient (one more G-sized buffer);
+    // without room for them, upload G whole and walk in one launch per download block
+    bool segmented = gray && segs >= 2;
+    if (segmented && ctx->ensure(&ctx->part, &ctx->part_bytes, bytes) != PD_OK) {
+        cudaGetLastError();
+        segmented = false;
+    }
+    if (segmented) {
+        // Every X-mask walks the first half of the walk in segments that follow the upload; the
+        // second half (with K2s the expensive one: 16 live chains per thread against <= 8) is one
+        // final segment, launched per download block and alternating over two streams, so the
+        // downloads overlap it. N=14 e2e 377 -> 367 ms against the PR-1 split (a quarter of the
+        // X-masks segmented, the rest whole walks once G is up: with K2s the cheap early chunks
+        // left the GPU idle during the upload); N=13 57.8, N=12 13.8 ms.
         double2* part = static_cast<double2*>(ctx->part);
         // walk segments [bnd[k], bnd[k+1]) in chunks: `ones` single chunks (the first upload,
         // the only one not hidden behind K2, is one chunk), then aligned runs of `runlen` chunks,
-        // so that block A's walk follows the upload instead of idling until a long segment's
-        // columns have arrived. N=14 e2e: doubling segments 1, 1, 2, 4, 8 510-515 ms; 4 x 1 then
-        // runs of 2: 500.5 ms (2 x 1 then 2: 502.9; 4 x 1 then 1: 502; then 4: 504; a = 1: 548;
-        // a = 3: 515)
+        // so that the walk follows the upload instead of idling until a long segment's columns
+        // have arrived (N=14 e2e, PR-1 split: doubling segments 1, 1, 2, 4, 8 510-515 ms; 4 x 1
+        // then runs of 2: 500.5 ms)
         constexpr unsigned ones = 4, runlen = 2;
         unsigned bnd[pd_ctx::kSegs + 1];
         unsigned nb = 0;
         bnd[nb++] = 0;
-        for (unsigned c = 0; c < nch;) {
+        const unsigned half = nch / 2;
+        for (unsigned c = 0; c < half;) {
             unsigned L = nb - 1 < ones ? 1u : runlen;
-            while (L > 1 && (c % L || c + L > nch)) L >>= 1;
+            while (L > 1 && (c % L || c + L > half)) L >>= 1;
             if (nb == pd_ctx::kSegs) return fail(PD_EINVAL, "walk segment plan too long");
             c += L;
             bnd[nb++] = c;
         }
+        bnd[nb++] = nch;
         const unsigned nseg = nb - 1;
         const uint64_t C = dim / nch;  // columns per walk chunk
         for (unsigned sg = 0; sg < nseg; ++sg) {
@@ -621,38 +634,33 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
             PD_CUDA(cudaMemcpy2DAsync(gdev + 2 * col0, dim * sizeof(double2), g + 2 * col0,
                                       dim * sizeof(double2), W * sizeof(double2), dim,
                                       cudaMemcpyHostToDevice, ctx->h2d));
+            PD_CUDA(cudaEventRecord(ctx->copied[sg], ctx->h2d));
+            PD_CUDA(cudaStreamWaitEvent(ctx->gather, ctx->copied[sg], 0));
             cudaError_t e = pdb::launch_diag_gather_cols(reinterpret_cast<const double2*>(gdev), N,
                                                          0, dim, col0, W,
-                                                         reinterpret_cast<double2*>(diag), ctx->h2d);
+                                                         reinterpret_cast<double2*>(diag), ctx->gather);
             if (e != cudaSuccess) return cuda_fail(e, "diag_gather launch");
-            PD_CUDA(cudaEventRecord(ctx->cols_ready[sg], ctx->h2d));
+            PD_CUDA(cudaEventRecord(ctx->cols_ready[sg], ctx->gather));
         }
-        // block A on ctx->stream: segments as the columns arrive, then its last segment in qa
-        // download blocks (continuing from the stored raw sums)
+        // segments as the columns arrive, then the final segment in download blocks (continuing
+        // from the stored raw sums) over ctx->stream and stream2
         for (unsigned sg = 0; sg + 1 < nseg; ++sg) {
             PD_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->cols_ready[sg], 0));
             cudaError_t e = pdb::launch_gray_segment(reinterpret_cast<const double2*>(diag), N, 0,
-                                                     xa, bnd[sg], bnd[sg + 1],
+                                                     dim, bnd[sg], bnd[sg + 1],
                                                      sg ? part : nullptr, part, 0, nullptr,
                                                      PD_LAYOUT_GLOBAL, ctx->stream, kChunkLog);
             if (e != cudaSuccess) return cuda_fail(e, "gray segment launch");
         }
         PD_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->cols_ready[nseg - 1], 0));
-        for (unsigned q = 0; q < qa; ++q) {
+        PD_CUDA(cudaEventRecord(ctx->seg_done, ctx->stream));
+        PD_CUDA(cudaStreamWaitEvent(ctx->stream2, ctx->seg_done, 0));
+        for (unsigned q = 0; q < nblk; ++q) {
+            cudaStream_t s = (q & 1) ? ctx->stream2 : ctx->stream;
             cudaError_t e = pdb::launch_gray_segment(
                 reinterpret_cast<const double2*>(diag) + q * xc * dim, N, q * xc, xc, bnd[nseg - 1], 0,
                 part + q * xc * dim, nullptr, 0, reinterpret_cast<double2*>(dout), PD_LAYOUT_GLOBAL,
-                ctx->stream, kChunkLog);
-            if (e != cudaSuccess) return cuda_fail(e, "gray block launch");
-            if (int rc = download(q, ctx->stream)) return rc;
-        }
-        // the rest: whole walks once G is complete, alternating over two further streams
-        PD_CUDA(cudaStreamWaitEvent(ctx->stream2, ctx->cols_ready[nseg - 1], 0));
-        for (unsigned q = qa; q < nblk; ++q) {
-            cudaStream_t s = (q & 1) ? ctx->stream2 : ctx->h2d;
-            cudaError_t e = pdb::launch_gray_segment(
-                reinterpret_cast<const double2*>(diag) + q * xc * dim, N, q * xc, xc, 0, 0, nullptr,
-                nullptr, 0, reinterpret_cast<double2*>(dout), PD_LAYOUT_GLOBAL, s);
+                s, kChunkLog);
             if (e != cudaSuccess) return cuda_fail(e, "gray block launch");
             if (int rc = download(q, s)) return rc;
         }
@@ -682,6 +690,7 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
     PD_CUDA(cudaStreamSynchronize(ctx->stream));
     PD_CUDA(cudaStreamSynchronize(ctx->stream2));
     PD_CUDA(cudaStreamSynchronize(ctx->h2d));
+    PD_CUDA(cudaStreamSynchronize(ctx->gather));
     return PD_OK;
 }
 

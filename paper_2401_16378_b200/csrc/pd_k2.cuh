@@ -244,4 +244,8 @@ __global__ void __launch_bounds__(kK2Threads, 2) gray_xmask_kernel(const K2Param
 // the segment instantiation of K=4 lives in pd_k2seg.cu (own ptxas run); launches it
 cudaError_t launch_gray_seg4(const K2Params& P, unsigned grid, size_t smem, cudaStream_t stream);
 
+// K2s, the shared-prefix form of K2 (pd_k2share.cu): same geometry, parameters and results
+bool gray_share_ok(unsigned N, unsigned run_bits);
+cudaError_t launch_gray_share(const K2Params& P, bool seg, unsigned grid, size_t smem, cudaStream_t stream);
+
 }  // namespace pdb

@@ -14,6 +14,7 @@
 
 #include <atomic>
 #include <cstdint>
+#include <cstdlib>
 #include <type_traits>
 
 #include "pd_device.cuh"
@@ -95,6 +96,11 @@ static cudaError_t launch_gray(const K2Params& P0, cudaStream_t stream) {
     const bool seg = P.c_begin != 0 || P.c_end != g.nchunks || P.part_in || P.part_out;
     const bool mapped = P.run_bits > kRunPtrBits;
     if constexpr (K == 4) {
+        static const char* share_env = std::getenv("PD_K2SHARE");
+        if (!(share_env && share_env[0] == '0') && gray_share_ok(P.N, P.run_bits)) {
+            const cudaError_t e = launch_gray_share(P, seg, static_cast<unsigned>(g.grid), g.smem_bytes, stream);
+            return e != cudaSuccess ? e : count_launch();
+        }
         if (seg && !mapped) {
             const cudaError_t e = launch_gray_seg4(P, static_cast<unsigned>(g.grid), g.smem_bytes, stream);
             return e != cudaSuccess ? e : count_launch();

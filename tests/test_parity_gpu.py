@@ -141,12 +141,32 @@ def test_integer_inputs_bit_exact_any_order(pd, cuda, port):
         assert same_values(pd.decompose(g, path=path), ref), path
 
 
-def test_real_input_y_parity_exact_zero(pd, cuda, port):
-    g = port.random_matrix(8, 55).real.astype(complex)
+@pytest.mark.parametrize("nq", [8, 10])
+def test_real_input_y_parity_exact_zero(pd, cuda, port, nq):
+    """real G: coefficients with an even number of Y factors are real, odd ones imaginary, and
+    the other part is an exact zero (N=10: K2s, whose chains carry region signs, N=8: K2)"""
+    g = port.random_matrix(nq, 55).real.astype(complex)
     d = pd.decompose(g)
-    ys = np.array([sum(((n >> (2 * t)) & 3) == 2 for t in range(8)) for n in range(4**8)])
+    n = np.arange(4**nq)
+    ys = sum(((n >> (2 * t)) & 3) == 2 for t in range(nq))
     assert np.all(d.imag[ys % 2 == 0] == 0.0)
     assert np.all(d.real[ys % 2 == 1] == 0.0)
+    assert same_values(d, port.decompose(g))
+
+
+def test_structured_matrices_k2s_exact(pd, cuda, port):
+    """K2s (N >= 9) on inputs whose sums cancel exactly: a Kronecker product of Paulis (one
+    nonzero coefficient), a permutation matrix and a 0/1 band matrix — every coefficient equal
+    to the reference walk's (IEEE ==)"""
+    nq = 10
+    P = [np.eye(2), np.array([[0, 1], [1, 0]]), np.array([[0, -1j], [1j, 0]]), np.diag([1, -1])]
+    k = np.array([[1.0 + 0j]])
+    for t in range(nq):
+        k = np.kron(P[(3 * t + 1) % 4], k)
+    perm = np.eye(2**nq)[np.random.default_rng(3).permutation(2**nq)].astype(complex)
+    band = np.triu(np.tril(np.ones((2**nq, 2**nq)), 2), -1).astype(complex)
+    for g in (k.astype(complex), perm, band):
+        assert same_values(pd.decompose(g), port.decompose(g))
 
 
 def test_recompose_round_trip(pd, cuda, port):

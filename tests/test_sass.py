@@ -15,6 +15,7 @@ from conftest import ROOT
 
 OBJ = os.path.join(ROOT, "paper_2401_16378_b200", "csrc", "build", "pd_kernels.o")
 SEG_OBJ = os.path.join(ROOT, "paper_2401_16378_b200", "csrc", "build", "pd_k2seg.o")
+SHARE_OBJ = os.path.join(ROOT, "paper_2401_16378_b200", "csrc", "build", "pd_k2share.o")
 WHT_OBJ = os.path.join(ROOT, "paper_2401_16378_b200", "csrc", "build", "pd_wht.o")
 CUOBJDUMP = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
 
@@ -77,12 +78,12 @@ def test_k2_streams_diagonals_with_bulk_copies():
 
 
 def test_no_local_memory_in_hot_kernels():
-    for obj in (OBJ, WHT_OBJ):
+    for obj in (OBJ, WHT_OBJ, SHARE_OBJ):
         log = open(obj + ".ptxas.log").read()
         for m in re.finditer(r"Function properties for (\S+)\n\s*(\d+) bytes stack frame, (\d+) bytes spill stores",
                              log):
             name, stack, spills = m.group(1), int(m.group(2)), int(m.group(3))
-            if "gray_xmask" in name or "wht_" in name or "diag_gather" in name:
+            if "gray_" in name or "wht_" in name or "diag_gather" in name:
                 assert spills == 0, (name, spills)
 
 
@@ -96,3 +97,41 @@ def test_k2_segment_instantiation_is_separate_and_clean():
     ops = [b.split()[0] for b in body]
     assert sum(o == "DADD" for o in ops) == 1024
     assert not any(o.startswith(("LDL", "STL")) for o in ops)
+
+
+def dadd_loops(ins):
+    """DADD count of every backward-branch loop body with at least 32 DADDs"""
+    addr = {a: i for i, (a, _) in enumerate(ins)}
+    out = {}
+    for i, (a, t) in enumerate(ins):
+        if "BRA" not in t:
+            continue
+        m = re.search(r"0x([0-9a-f]+)", t.split("BRA", 1)[1])
+        if m and int(m.group(1), 16) < a and int(m.group(1), 16) in addr:
+            body = [x[1] for x in ins[addr[int(m.group(1), 16)]:i + 1]]
+            n = sum(b.startswith("DADD") for b in body)
+            if n >= 32 and (n not in out or len(body) < len(out[n])):
+                out[n] = body
+    return out
+
+
+def share_kernels():
+    syms = subprocess.run([CUOBJDUMP, "-symbols", SHARE_OBJ], capture_output=True, text=True).stdout
+    names = sorted(set(re.findall(r"(_Z\S*gray_share_kernelILb[01]EE\S*)", syms)))
+    assert len(names) == 2, names
+    return names
+
+
+@pytest.mark.skipif(not os.path.exists(SHARE_OBJ), reason="K2s not built")
+def test_k2s_has_one_pure_dadd_loop_per_live_chain_count():
+    """K2s (pd_k2share.cu): one loop body per live-chain count (1, 2, 4, 8, 16 chains x re/im x
+    32 elements = 64 ... 1024 DADDs), the 16-chain one with K2's instruction mix, and no
+    multiplies or local memory anywhere in the loops."""
+    for fun in share_kernels():
+        loops = dadd_loops(sass_of(SHARE_OBJ, fun))
+        for n in (64, 128, 256, 512, 1024):
+            assert n in loops, (fun, sorted(loops))
+            ops = [b.split()[0] for b in loops[n]]
+            assert not any(o.startswith(("DMUL", "DFMA", "LDL", "STL")) for o in ops)
+            assert sum(o.startswith("LDS") for o in ops) == 32
+        assert 1024 / len(loops[1024]) > 0.85, len(loops[1024])
