@@ -18,11 +18,11 @@ CMDS = """```
 python bench.py --steps 3 --warmup 3 --no-cpu-baseline && \\
 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline
 C1="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-extras"
-ncu --set full --clock-control none --import-source on -k regex:"gray_xmask|diag_gather" -c 2 -o prof_gray $C1
+ncu --set full --clock-control none --import-source on -k regex:"gray_share|diag_gather" -c 2 -o prof_gray $C1
 C2="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-extras --path wht"
 ncu --set full --clock-control none --import-source on -k regex:"wht" -s 300 -c 2 -o prof_wht $C2
 ncu --replay-mode range --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,lts__t_sector_hit_rate.pct \\
-    python gpurun_exp/wht_range.py <lib>        (PD_PATH=1 WHT, PD_PATH=0 Gray: one pd_decompose_device call)
+    python profiles/scripts/wht_range.py <lib>        (PD_PATH=1 WHT, PD_PATH=0 Gray: one pd_decompose_device call)
 ```"""
 
 
@@ -30,10 +30,13 @@ def main():
     b = json.load(open(os.path.join(HERE, "r01_bench_final.json")))
     r, w, sc, cb = b["roofline"], b["wht_path"], b["side_configs"], b["cpu_baseline"]
     rows = [
-        ("N=14 Gray path (K1+K2), device-resident",
+        ("N=14 Gray path (K1+K2s), device-resident",
          f"{b['ms_per_step']:.2f} ms/step = {b['value'] / 1e6:.1f} M coeff/s"),
-        ("K2 roofline", f"{r['achieved']:.2f} of {r['peak']:.2f} TFLOP/s nominal FP64-add = **{100 * r['frac']:.1f} %** "
+        ("K2s roofline (DADDs executed)", f"{r['achieved']:.2f} of {r['peak']:.2f} TFLOP/s nominal FP64-add = **{100 * r['frac']:.1f} %** "
                         f"({100 * r['frac_of_probe']:.1f} % of the live DADD probe, {r['probe_tflops']:.2f})"),
+        ("K2s in reference-walk adds", f"{r['reference_walk_equiv_tflops']:.2f} TFLOP/s: the reference's 2 x 8^N adds "
+                                       f"over K2s' time ({100 * r['reference_walk_equiv_tflops'] / r['peak']:.0f} % of the "
+                                       f"FP64-add peak; K2s skips the shared walk prefixes)"),
         ("K1 diagonal gather", f"{r['k1_gather_ms']:.3f} ms = {r['k1_gather_gbs']:.0f} GB/s "
                                f"({100 * r['k1_gather_gbs'] / 6542.7:.1f} % of measured 6542.7)"),
         ("e2e `decompose(pinned host G, out=pinned host)`",
@@ -55,18 +58,18 @@ def main():
     t = json.load(open(os.path.join(HERE, "ncu_traffic.json")))
     out = ["# Round 1 ncu evidence (B200, N=14 full decomposition)", "",
            "Commands (each run only after the same command exited 0 without ncu, "
-           "`gpurun_exp/round_evidence.sh`):", "", CMDS, "",
+           "`profiles/scripts/round_evidence.sh`):", "", CMDS, "",
            "## Headline (bench.py default, `r01_bench_final.json`)", "", "| quantity | value |", "|---|---|"]
     out += [f"| {k} | {v} |" for k, v in rows]
     out += ["", "## DRAM traffic of a whole decomposition (range replay)", "",
-            f"* Gray (K1 + K2): {t['N14_gray_range_read'] / 1e9:.2f} GB read + {t['N14_gray_range_write'] / 1e9:.2f} GB "
-            f"written (algorithmic: K1 8.59 GB + K2 8.59 GB).",
+            f"* Gray (K1 + K2s): {t['N14_gray_range_read'] / 1e9:.2f} GB read + {t['N14_gray_range_write'] / 1e9:.2f} GB "
+            f"written (algorithmic: K1 8.59 GB + K2s 8.59 GB).",
             f"* WHT chunked: {t['N14_wht_range_read'] / 1e9:.2f} GB read + {t['N14_wht_range_write'] / 1e9:.2f} GB written "
             f"(algorithmic 8.59 GB; the one-chunk design moved 17.1 GB). D' never leaves L2.", "",
             "## Launch list of the default bench command (cold-cache, serialised — compare shares)", "",
             launches(os.path.join(HERE, "r01_launches_N14_bench.csv")), "",
-            "(`gray_xmask_kernel<4,1,0>` is the segmented K2 of the pipelined host path inside the e2e "
-            "measurement; `<4,0,0>` the device-resident one; the WHT kernels run once per 64-X-mask chunk (16 MiB of D'), "
+            "(`gray_share_kernel<1>` is the segmented K2s of the pipelined host path inside the e2e "
+            "measurement; `<0>` the device-resident one; the WHT kernels run once per 64-X-mask chunk (16 MiB of D'), "
             "the strings kernels once per configs[1] batch.)", "",
             "## Full-set captures", "",
             report(os.path.join(HERE, "r01_prof_gray_N14.ncu-rep")), "",
