@@ -32,6 +32,7 @@
 
 #include <atomic>
 #include <cstdint>
+#include <cstdlib>
 
 #include "pd_k2.cuh"
 
