@@ -345,7 +345,8 @@ def run_ours(args) -> None:
         ref_dadd = 2.0 * dim * (4**nq / world)  # the reference's walk: 2 adds x 2^N terms each
         achieved = dadd / (k2_ms / 1e3) / 1e12
         peak = SM_COUNT * FP64_LANES_PER_SM * sm_max * 1e6 / 1e12
-        roofline = {"bound": "fp64", "kernel": "gray_share_kernel (K2s)", "achieved": achieved,
+        roofline = {"bound": "fp64", "kernel": "gray_share_c_kernel (K2s-c)" if nq >= 13 else "gray_share_kernel (K2s)",
+                    "achieved": achieved,
                     "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                     "algorithmic": f"DADDs K2s executes: the reference's 2*2^N per coefficient less the "
                                    f"shared walk prefixes (x 171/256) = {dadd:.4g} per launch",

@@ -1,0 +1,68 @@
+"""K2s kernel forms against each other, bit for bit, over the whole coefficient array.
+
+The Gray path has three kernels that must agree exactly: K2 (PD_K2SHARE=0: every chain
+computed in full), K2s with per-thread sign words (PD_K2S_C=0; N in [9, 12] always) and K2s-c,
+whose CTAs share the low four Z-mask bits as a compile-time constant (N >= 13). The
+kernel choice is read once per process, so each form runs in its own subprocess."""
+import hashlib
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2401_16378_b200 as pd
+nq, kind, path = int(sys.argv[2]), sys.argv[3], sys.argv[4]
+d = 2 ** nq
+rng = np.random.default_rng(900 + nq)
+if kind == "normal":
+    g = rng.standard_normal((d, d)) + 1j * rng.standard_normal((d, d))
+elif kind == "band":      # 0/1 band: exact cancellations, exact zeros
+    g = np.triu(np.tril(np.ones((d, d)), 2), -1).astype(complex)
+else:                     # small integers: every partial sum exact
+    g = (rng.integers(-3, 4, (d, d)) + 1j * rng.integers(-3, 4, (d, d))).astype(complex)
+gd = torch.from_numpy(g).to("cuda:0")
+out = torch.empty(4 ** nq, dtype=torch.complex128, device="cuda:0")
+scr = torch.empty_like(out)
+if path == "device":
+    pd.device.decompose(nq, gd.data_ptr(), out.data_ptr(), scr.data_ptr(), "gray", 0)
+    torch.cuda.synchronize()
+    res = out.cpu().numpy()
+else:                     # host buffers: the segmented pipeline (partial sums across launches)
+    res = pd.decompose(g)
+np.save(sys.argv[5], res)
+"""
+
+
+def run(tmp_path, nq, kind, path, env):
+    f = tmp_path / f"{nq}_{kind}_{path}_{'_'.join(f'{k}{v}' for k, v in env.items())}.npy"
+    e = dict(os.environ, **env)
+    subprocess.run([sys.executable, "-c", SCRIPT, ROOT, str(nq), kind, path, str(f)], env=e, check=True,
+                   timeout=600)
+    return np.load(f)
+
+
+@pytest.mark.parametrize("nq,kind", [(13, "normal"), (13, "band"), (13, "int"), (14, "band")])
+def test_k2s_c_bitwise_equal_sign_word_form(cuda, tmp_path, nq, kind):
+    u = run(tmp_path, nq, kind, "device", {})
+    w = run(tmp_path, nq, kind, "device", {"PD_K2S_C": "0"})
+    assert u.tobytes() == w.tobytes()
+    if nq <= 13:  # and K2 (full chains): equal values (an exact zero's sign may differ)
+        k2 = run(tmp_path, nq, kind, "device", {"PD_K2SHARE": "0"})
+        assert np.all(u == k2)
+
+
+@pytest.mark.parametrize("nq", [13, 14])
+def test_k2s_c_host_pipeline_segments(cuda, tmp_path, nq):
+    """host buffers: walk segments that stop and restart mid-walk from stored raw sums"""
+    u = run(tmp_path, nq, "normal", "host", {})
+    w = run(tmp_path, nq, "normal", "device", {"PD_K2S_C": "0"})
+    assert u.tobytes() == w.tobytes()

@@ -135,3 +135,30 @@ def test_k2s_has_one_pure_dadd_loop_per_live_chain_count():
             assert not any(o.startswith(("DMUL", "DFMA", "LDL", "STL")) for o in ops)
             assert sum(o.startswith("LDS") for o in ops) == 32
         assert 1024 / len(loops[1024]) > 0.85, len(loops[1024])
+
+
+@pytest.mark.skipif(not os.path.exists(SHARE_OBJ), reason="K2s not built")
+def test_k2s_c_has_sixteen_zlo_bodies_with_k2_loops():
+    """K2s-c (N >= 13): one body per compile-time ZLO (16), each with the five live-chain loops;
+    the element signs are DADD operand modifiers, so the 16-chain loop has K2's mix (1024 DADD,
+    32 LDS.128, no 3-input sign-word LOP3) and there are no multiplies or local memory."""
+    syms = subprocess.run([CUOBJDUMP, "-symbols", SHARE_OBJ], capture_output=True, text=True).stdout
+    names = sorted(set(re.findall(r"(_Z\S*gray_share_c_kernelILb[01]EE\S*)", syms)))
+    assert len(names) == 2, names
+    for fun in names:
+        ins = sass_of(SHARE_OBJ, fun)
+        addr = {a: i for i, (a, _) in enumerate(ins)}
+        hot = []
+        for i, (a, t) in enumerate(ins):
+            m = re.search(r"0x([0-9a-f]+)", t.split("BRA", 1)[1]) if "BRA" in t else None
+            if m and int(m.group(1), 16) < a and int(m.group(1), 16) in addr:
+                body = [x[1] for x in ins[addr[int(m.group(1), 16)]:i + 1]]
+                if sum(b.startswith("DADD") for b in body) == 1024:
+                    hot.append(body)
+        assert len(hot) == 16, (fun, len(hot))
+        for body in hot:
+            ops = [b.split()[0] for b in body]
+            assert sum(o.startswith("LDS") for o in ops) == 32
+            assert not any(o.startswith(("DMUL", "DFMA", "LDL", "STL")) for o in ops)
+            assert not any(b.startswith("LOP3") and "0x96" in b for b in body)
+            assert len(body) <= 1210, len(body)
