@@ -519,6 +519,38 @@ int pd_first_nonfinite_device(const double* g, uint64_t count, uint64_t* first, 
 
 namespace {
 
+// Opt-in timeline of the pipelined host path (PD_E2E_TIMELINE=1): CUDA events recorded after
+// each stage on the stream that ran it, printed to stderr as ms from the first upload once the
+// call has synchronised (profiles/r01_e2e_timeline.txt). Off by default: no events are recorded.
+struct HostTimeline {
+    bool on = false;
+    std::vector<std::pair<std::string, cudaEvent_t>> marks;
+    HostTimeline() {
+        const char* e = std::getenv("PD_E2E_TIMELINE");
+        on = e && e[0] == '1';
+    }
+    void mark(const std::string& name, cudaStream_t s) {
+        if (!on) return;
+        cudaEvent_t ev = nullptr;
+        if (cudaEventCreate(&ev) != cudaSuccess) return;
+        cudaEventRecord(ev, s);
+        marks.emplace_back(name, ev);
+    }
+    void report() {
+        if (!on || marks.empty()) return;
+        for (auto& m : marks) cudaEventSynchronize(m.second);
+        for (auto& m : marks) {
+            float ms = 0.f;
+            const cudaError_t e = cudaEventElapsedTime(&ms, marks.front().second, m.second);
+            std::fprintf(stderr, "TL %-12s %9.2f%s%s\n", m.first.c_str(), ms, e ? " " : "",
+                         e ? cudaGetErrorString(e) : "");
+        }
+    }
+    ~HostTimeline() {
+        for (auto& m : marks) cudaEventDestroy(m.second);
+    }
+};
+
 // the host-buffer decomposition; out == nullptr leaves the coefficients in ctx->out
 int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_path path) {
     const size_t bytes = elems(N) * sizeof(double2);
@@ -572,6 +604,7 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
     double* diag = static_cast<double*>(ctx->scratch);
     double* gdev = static_cast<double*>(ctx->g);
     const bool gray = path == PD_PATH_GRAY;
+    HostTimeline tl;
     // the host pipeline walks in chunks of 1024 columns (half K2's default) so that the first,
     // exposed upload is 1/16 of G at N=14
     constexpr unsigned kChunkLog = 10;  // 9 and 11 measured 500.5 and 508 ms (N=14 e2e)
@@ -626,6 +659,7 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
         bnd[nb++] = nch;
         const unsigned nseg = nb - 1;
         const uint64_t C = dim / nch;  // columns per walk chunk
+        tl.mark("start", ctx->h2d);
         for (unsigned sg = 0; sg < nseg; ++sg) {
             // an aligned run of L chunks visits the aligned run of L column chunks holding gray(b)
             const uint64_t L = bnd[sg + 1] - bnd[sg];
@@ -635,6 +669,7 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
                                       dim * sizeof(double2), W * sizeof(double2), dim,
                                       cudaMemcpyHostToDevice, ctx->h2d));
             PD_CUDA(cudaEventRecord(ctx->copied[sg], ctx->h2d));
+            tl.mark("up" + std::to_string(sg), ctx->h2d);
             PD_CUDA(cudaStreamWaitEvent(ctx->gather, ctx->copied[sg], 0));
             cudaError_t e = pdb::launch_diag_gather_cols(reinterpret_cast<const double2*>(gdev), N,
                                                          0, dim, col0, W,
@@ -651,6 +686,7 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
                                                      sg ? part : nullptr, part, 0, nullptr,
                                                      PD_LAYOUT_GLOBAL, ctx->stream, kChunkLog);
             if (e != cudaSuccess) return cuda_fail(e, "gray segment launch");
+            tl.mark("seg" + std::to_string(sg), ctx->stream);
         }
         PD_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->cols_ready[nseg - 1], 0));
         PD_CUDA(cudaEventRecord(ctx->seg_done, ctx->stream));
@@ -662,7 +698,9 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
                 part + q * xc * dim, nullptr, 0, reinterpret_cast<double2*>(dout), PD_LAYOUT_GLOBAL,
                 s, kChunkLog);
             if (e != cudaSuccess) return cuda_fail(e, "gray block launch");
+            tl.mark("blk" + std::to_string(q), s);
             if (int rc = download(q, s)) return rc;
+            tl.mark("d2h" + std::to_string(q), ctx->d2h);
         }
     } else {
         if (int rc = upload(ctx, ctx->g, g, bytes)) return rc;
@@ -691,6 +729,7 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
     PD_CUDA(cudaStreamSynchronize(ctx->stream2));
     PD_CUDA(cudaStreamSynchronize(ctx->h2d));
     PD_CUDA(cudaStreamSynchronize(ctx->gather));
+    tl.report();
     return PD_OK;
 }
 

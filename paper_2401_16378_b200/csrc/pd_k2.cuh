@@ -247,5 +247,8 @@ cudaError_t launch_gray_seg4(const K2Params& P, unsigned grid, size_t smem, cuda
 // K2s, the shared-prefix form of K2 (pd_k2share.cu): same geometry, parameters and results
 bool gray_share_ok(unsigned N, unsigned run_bits);
 cudaError_t launch_gray_share(const K2Params& P, bool seg, unsigned grid, size_t smem, cudaStream_t stream);
+// K2s-c (pd_k2share.cuh), whole walk (pd_k2c.cu) and walk segments (pd_k2cseg.cu); P in K2s-c geometry
+cudaError_t launch_gray_share_c_full(const K2Params& P, unsigned grid, cudaStream_t stream);
+cudaError_t launch_gray_share_c_seg(const K2Params& P, unsigned grid, cudaStream_t stream);
 
 }  // namespace pdb

@@ -1,0 +1,11 @@
+// pd_k2c.cu — the K2s-c kernel for whole walk, in its own translation unit so that
+// ptxas allocates it separately from the other instantiation (pd_k2share.cuh).
+#include "pd_k2share.cuh"
+
+namespace pdb {
+
+cudaError_t launch_gray_share_c_full(const K2Params& P, unsigned grid, cudaStream_t stream) {
+    return launch_gray_share_c_impl<false>(P, grid, stream);
+}
+
+}  // namespace pdb

@@ -27,6 +27,9 @@ cudaError_t launch_gray_segment(const double2* diag, unsigned N, uint64_t x0, ui
                                 double2* part_out, unsigned run_bits, double2* out, int layout,
                                 cudaStream_t stream, unsigned chunk_log = 0);
 unsigned gray_xmask_chunks(unsigned N);  // walk chunks per diagonal (1 for N < 12)
+// fewest X-masks per Gray launch for which K2s-c (N >= 13) is used: each of its 16 compile-time
+// bodies must span more CTAs than the GPU holds at once (smaller launches take K2s)
+uint64_t gray_share_c_min_xmasks(unsigned N);
 
 // K2: Gray-code sums for the X-masks [x0, x0 + x_count); output layout as in pd_api.h
 cudaError_t launch_gray_xmask(const double2* diag, unsigned N, uint64_t x0, uint64_t x_count,

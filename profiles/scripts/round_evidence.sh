@@ -1,6 +1,7 @@
 #!/bin/bash
 # tests, smoke, bench, launch list and full ncu captures of the top kernels (one GPU)
 set -x
+rm -rf /tmp/pytest-of-root  # a reused box keeps /tmp
 python -m pytest tests -m gpu -x -q > gpurun_out/ev_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/ev_pytest.log
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/ev_smoke.log 2>&1
 python bench.py > gpurun_out/ev_bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/ev_bench.log

@@ -16,6 +16,8 @@ from conftest import ROOT
 OBJ = os.path.join(ROOT, "paper_2401_16378_b200", "csrc", "build", "pd_kernels.o")
 SEG_OBJ = os.path.join(ROOT, "paper_2401_16378_b200", "csrc", "build", "pd_k2seg.o")
 SHARE_OBJ = os.path.join(ROOT, "paper_2401_16378_b200", "csrc", "build", "pd_k2share.o")
+C_OBJ = os.path.join(ROOT, "paper_2401_16378_b200", "csrc", "build", "pd_k2c.o")
+CSEG_OBJ = os.path.join(ROOT, "paper_2401_16378_b200", "csrc", "build", "pd_k2cseg.o")
 WHT_OBJ = os.path.join(ROOT, "paper_2401_16378_b200", "csrc", "build", "pd_wht.o")
 CUOBJDUMP = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
 
@@ -78,7 +80,7 @@ def test_k2_streams_diagonals_with_bulk_copies():
 
 
 def test_no_local_memory_in_hot_kernels():
-    for obj in (OBJ, WHT_OBJ, SHARE_OBJ):
+    for obj in (OBJ, WHT_OBJ, SHARE_OBJ, C_OBJ, CSEG_OBJ):
         log = open(obj + ".ptxas.log").read()
         for m in re.finditer(r"Function properties for (\S+)\n\s*(\d+) bytes stack frame, (\d+) bytes spill stores",
                              log):
@@ -137,16 +139,19 @@ def test_k2s_has_one_pure_dadd_loop_per_live_chain_count():
         assert 1024 / len(loops[1024]) > 0.85, len(loops[1024])
 
 
-@pytest.mark.skipif(not os.path.exists(SHARE_OBJ), reason="K2s not built")
+@pytest.mark.skipif(not os.path.exists(CSEG_OBJ), reason="K2s-c not built")
 def test_k2s_c_has_sixteen_zlo_bodies_with_k2_loops():
     """K2s-c (N >= 13): one body per compile-time ZLO (16), each with the five live-chain loops;
     the element signs are DADD operand modifiers, so the 16-chain loop has K2's mix (1024 DADD,
     32 LDS.128, no 3-input sign-word LOP3) and there are no multiplies or local memory."""
-    syms = subprocess.run([CUOBJDUMP, "-symbols", SHARE_OBJ], capture_output=True, text=True).stdout
-    names = sorted(set(re.findall(r"(_Z\S*gray_share_c_kernelILb[01]EE\S*)", syms)))
-    assert len(names) == 2, names
-    for fun in names:
-        ins = sass_of(SHARE_OBJ, fun)
+    found = []
+    for obj in (C_OBJ, CSEG_OBJ):  # one instantiation per translation unit
+        syms = subprocess.run([CUOBJDUMP, "-symbols", obj], capture_output=True, text=True).stdout
+        names = sorted(set(re.findall(r"(_Z\S*gray_share_c_kernelILb[01]EE\S*)", syms)))
+        assert len(names) == 1, (obj, names)
+        found.append((obj, names[0]))
+    for obj, fun in found:
+        ins = sass_of(obj, fun)
         addr = {a: i for i, (a, _) in enumerate(ins)}
         hot = []
         for i, (a, t) in enumerate(ins):
