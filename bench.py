@@ -348,7 +348,7 @@ def run_ours(args) -> None:
         roofline = {"bound": "fp64", "kernel": "gray_share_c_kernel (K2s-c)" if nq >= 13 else "gray_share_kernel (K2s)",
                     "achieved": achieved,
                     "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
-                    "algorithmic": f"DADDs K2s executes: the reference's 2*2^N per coefficient less the "
+                    "algorithmic": f"DADDs the Gray kernel executes: the reference's 2*2^N per coefficient less the "
                                    f"shared walk prefixes (x 171/256) = {dadd:.4g} per launch",
                     "reference_walk_equiv_tflops": ref_dadd / (k2_ms / 1e3) / 1e12,
                     "peak_source": f"nominal FP64 add: {SM_COUNT} SM x {FP64_LANES_PER_SM} lanes x "

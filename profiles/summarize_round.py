@@ -30,15 +30,15 @@ def main():
     b = json.load(open(os.path.join(HERE, "r01_bench_final.json")))
     r, w, sc, cb = b["roofline"], b["wht_path"], b["side_configs"], b["cpu_baseline"]
     rows = [
-        ("N=14 Gray path (K1+K2s), device-resident",
+        ("N=14 Gray path (K1+K2s-c), device-resident",
          f"{b['ms_per_step']:.2f} ms/step = {b['value'] / 1e6:.1f} M coeff/s"),
-        ("K2s roofline (DADDs executed)", f"{r['achieved']:.2f} of {r['peak']:.2f} TFLOP/s nominal FP64-add = **{100 * r['frac']:.1f} %** "
+        ("K2s-c roofline (DADDs executed)", f"{r['achieved']:.2f} of {r['peak']:.2f} TFLOP/s nominal FP64-add = **{100 * r['frac']:.1f} %** "
                         f"({100 * r['frac_of_probe']:.1f} % of the live DADD probe, {r['probe_tflops']:.2f})"),
-        ("K2s in reference-walk adds", f"{r['reference_walk_equiv_tflops']:.2f} TFLOP/s: the reference's 2 x 8^N adds "
-                                       f"over K2s' time ({100 * r['reference_walk_equiv_tflops'] / r['peak']:.0f} % of the "
-                                       f"FP64-add peak; K2s skips the shared walk prefixes)"),
+        ("K2s-c in reference-walk adds", f"{r['reference_walk_equiv_tflops']:.2f} TFLOP/s: the reference's 2 x 8^N adds "
+                                       f"over K2s-c's time ({100 * r['reference_walk_equiv_tflops'] / r['peak']:.0f} % of the "
+                                       f"FP64-add peak; K2s-c skips the shared walk prefixes)"),
         ("K1 diagonal gather", f"{r['k1_gather_ms']:.3f} ms = {r['k1_gather_gbs']:.0f} GB/s "
-                               f"({100 * r['k1_gather_gbs'] / 6542.7:.1f} % of measured 6542.7)"),
+                               f"({100 * r['k1_gather_gbs'] / w['roofline']['peak']:.1f} % of the measured {w['roofline']['peak']:g})"),
         ("e2e `decompose(pinned host G, out=pinned host)`",
          f"{b['e2e']['ms_per_step']:.1f} ms = {b['e2e']['value'] / 1e6:.1f} M coeff/s (8 GiB of H2D+D2H inside)"),
         ("WHT path (chunked L2-resident two-pass)",
@@ -62,14 +62,17 @@ def main():
            "## Headline (bench.py default, `r01_bench_final.json`)", "", "| quantity | value |", "|---|---|"]
     out += [f"| {k} | {v} |" for k, v in rows]
     out += ["", "## DRAM traffic of a whole decomposition (range replay)", "",
-            f"* Gray (K1 + K2s): {t['N14_gray_range_read'] / 1e9:.2f} GB read + {t['N14_gray_range_write'] / 1e9:.2f} GB "
-            f"written (algorithmic: K1 8.59 GB + K2s 8.59 GB).",
+            f"* Gray (K1 + K2s-c): {t['N14_gray_range_read'] / 1e9:.2f} GB read + {t['N14_gray_range_write'] / 1e9:.2f} GB "
+            f"written (algorithmic: K1 8.59 GB + K2s-c 8.59 GB). K2s-c streams the diagonals D (4.3 GB) once per "
+            f"compile-time ZLO phase (16 x): ~218 GB/s, 3 % of HBM, on a kernel bound by the FP64 pipe; one "
+            f"ZLO body at a time is what makes it fast (`r01_k2s_c.md`).",
             f"* WHT chunked: {t['N14_wht_range_read'] / 1e9:.2f} GB read + {t['N14_wht_range_write'] / 1e9:.2f} GB written "
             f"(algorithmic 8.59 GB; the one-chunk design moved 17.1 GB). D' never leaves L2.", "",
             "## Launch list of the default bench command (cold-cache, serialised — compare shares)", "",
             launches(os.path.join(HERE, "r01_launches_N14_bench.csv")), "",
-            "(`gray_share_kernel<1>` is the segmented K2s of the pipelined host path inside the e2e "
-            "measurement; `<0>` the device-resident one; the WHT kernels run once per 64-X-mask chunk (16 MiB of D'), "
+            "(`gray_share_c_kernel<0>` is the device-resident Gray kernel (K2s-c); `gray_share_c_kernel<1>` and "
+            "`gray_share_kernel<1>` are the walk segments of the pipelined host path inside the e2e measurement (the "
+            "512-X-mask final blocks take K2s); the WHT kernels run once per 64-X-mask chunk (16 MiB of D'), "
             "the strings kernels once per configs[1] batch.)", "",
             "## Full-set captures", "",
             report(os.path.join(HERE, "r01_prof_gray_N14.ncu-rep")), "",
