@@ -637,7 +637,11 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
         // final segment, launched per download block and alternating over two streams, so the
         // downloads overlap it. N=14 e2e 377 -> 367 ms against the PR-1 split (a quarter of the
         // X-masks segmented, the rest whole walks once G is up: with K2s the cheap early chunks
-        // left the GPU idle during the upload); N=13 57.8, N=12 13.8 ms.
+        // left the GPU idle during the upload); N=13 57.8, N=12 13.8 ms. The first-half segments
+        // store raw sums and run K2q (pd_k2q.cu: 4 or 2 Z-masks per thread, so their few live
+        // chains are not latency-bound while they run alone during the upload): N=14 364 -> 355.5,
+        // N=13 59 -> 52.5 ms. Grouping the final blocks into launches large enough for K2s-c
+        // measured no gain at N=14 (355.5) and a loss at N=13 (59.3 ms), so they stay per block.
         double2* part = static_cast<double2*>(ctx->part);
         // walk segments [bnd[k], bnd[k+1]) in chunks: `ones` single chunks (the first upload,
         // the only one not hidden behind K2, is one chunk), then aligned runs of `runlen` chunks,

@@ -250,5 +250,9 @@ cudaError_t launch_gray_share(const K2Params& P, bool seg, unsigned grid, size_t
 // K2s-c (pd_k2share.cuh), whole walk (pd_k2c.cu) and walk segments (pd_k2cseg.cu); P in K2s-c geometry
 cudaError_t launch_gray_share_c_full(const K2Params& P, unsigned grid, cudaStream_t stream);
 cudaError_t launch_gray_share_c_seg(const K2Params& P, unsigned grid, cudaStream_t stream);
+// K2q (pd_k2q.cu): early walk segments (raw sums out, ending in region <= 7) with Q = 4 or 2
+// Z-masks per thread; gray_share_q_pick returns Q or 0. P in K2 geometry.
+unsigned gray_share_q_pick(const K2Params& P);
+cudaError_t launch_gray_share_q(const K2Params& P, unsigned q, cudaStream_t stream);
 
 }  // namespace pdb

@@ -1,4 +1,4 @@
-// pd_k2cseg.cu — the K2s-c kernel for walk segments (raw partial sums in/out), in its own translation unit so that
+// pd_k2cseg.cu — the K2s-c kernel for final walk segments (raw partial sums in, coefficients out), in its own translation unit so that
 // ptxas allocates it separately from the other instantiation (pd_k2share.cuh).
 #include "pd_k2share.cuh"
 

@@ -216,8 +216,12 @@ cudaError_t launch_gray_share(const K2Params& P0, bool seg, unsigned grid, size_
         if (e != cudaSuccess) return e;
         attr_set.fetch_or(1ull << dev);
     }
+    static const char* q_env = std::getenv("PD_K2Q");
+    if (seg && !(q_env && q_env[0] == '0'))
+        if (const unsigned q = gray_share_q_pick(P0)) return launch_gray_share_q(P0, q, stream);
     static const char* c_env = std::getenv("PD_K2S_C");
-    if (P0.N >= 13 && !(c_env && c_env[0] == '0') && P0.x_count >= gray_share_c_min_xmasks(P0.N)) {
+    if (P0.N >= 13 && !(c_env && c_env[0] == '0') && P0.part_out == nullptr &&
+        P0.x_count >= gray_share_c_min_xmasks(P0.N)) {
         // K2s-c geometry; the caller's chunks (2^ci_log steps) become 2^(ci_log - cs_log) stages
         K2Params P = P0;
         const unsigned tb = P0.N - 8 < 6 ? P0.N - 8 : 6;  // Z-mask bits 4 .. 4+tb-1 from the thread

@@ -245,12 +245,6 @@ __device__ __forceinline__ void share_body_c(const K2Params& P, const CtaC& t, u
         if (live <= static_cast<unsigned>(w))
 #pragma unroll
             for (int j = 0; j < w; ++j) ar[j + w] = ar[j], ai[j + w] = ai[j];
-    if (SEG && P.part_out != nullptr) {
-        double2* dst = P.part_out + xl * dim + (zm << 4);
-#pragma unroll
-        for (int j = 0; j < kChains; ++j) dst[j] = make_double2(ar[j], ai[j]);
-        return;
-    }
     const unsigned low_bits = 2 * (N - P.run_bits);
     const uint64_t low_mask = (low_bits >= 64) ? ~0ull : ((1ull << low_bits) - 1);
 #pragma unroll
@@ -318,7 +312,9 @@ __global__ void __launch_bounds__(kCThreads, 2) gray_share_c_kernel(const K2Para
     }
 }
 
-// one instantiation per translation unit (pd_k2c.cu: SEG = false, pd_k2cseg.cu: SEG = true)
+// one instantiation per translation unit (pd_k2c.cu: SEG = false, pd_k2cseg.cu: SEG = true). The SEG
+// form continues a walk from raw sums (part_in) and ends with the coefficients: segments that
+// store raw sums go to K2q or K2s (launch_gray_share).
 template <bool SEG>
 cudaError_t launch_gray_share_c_impl(const K2Params& P, unsigned grid, cudaStream_t stream) {
     static std::atomic<uint64_t> attr_set{0};  // one bit per device

@@ -1,9 +1,10 @@
 """K2s kernel forms against each other, bit for bit, over the whole coefficient array.
 
-The Gray path has three kernels that must agree exactly: K2 (PD_K2SHARE=0: every chain
+The Gray path has four kernels that must agree exactly: K2 (PD_K2SHARE=0: every chain
 computed in full), K2s with per-thread sign words (PD_K2S_C=0; N in [9, 12] always) and K2s-c,
-whose CTAs share the low four Z-mask bits as a compile-time constant (N >= 13). The
-kernel choice is read once per process, so each form runs in its own subprocess."""
+whose CTAs share the low four Z-mask bits as a compile-time constant (N >= 13), and K2q for
+the host pipeline's first walk segments (PD_K2Q=0 turns it off). The kernel choice is read
+once per process, so each form runs in its own subprocess."""
 import os
 import subprocess
 import sys
@@ -61,9 +62,13 @@ def test_k2s_c_bitwise_equal_sign_word_form(cuda, nq, kind):
         assert u[1] == k2[1]
 
 
-@pytest.mark.parametrize("nq", [13, 14])
-def test_k2s_c_host_pipeline_segments(cuda, nq):
-    """host buffers: walk segments that stop and restart mid-walk from stored raw sums"""
-    u = run(nq, "normal", "host", {})
-    w = run(nq, "normal", "device", {"PD_K2S_C": "0"})
+@pytest.mark.parametrize("nq,kind", [(12, "normal"), (13, "normal"), (13, "band"), (14, "normal")])
+def test_host_pipeline_segments_bitwise(cuda, nq, kind):
+    """host buffers: walk segments that stop and restart mid-walk from stored raw sums — the
+    first-half segments on K2q (4 and 2 Z-masks per thread), the rest on K2s — against one
+    whole-walk launch of the sign-word kernel, and against the same pipeline without K2q"""
+    u = run(nq, kind, "host", {})
+    w = run(nq, kind, "device", {"PD_K2S_C": "0"})
     assert u[0] == w[0]
+    if nq <= 13:
+        assert u[0] == run(nq, kind, "host", {"PD_K2Q": "0"})[0]

@@ -18,6 +18,7 @@ SEG_OBJ = os.path.join(ROOT, "paper_2401_16378_b200", "csrc", "build", "pd_k2seg
 SHARE_OBJ = os.path.join(ROOT, "paper_2401_16378_b200", "csrc", "build", "pd_k2share.o")
 C_OBJ = os.path.join(ROOT, "paper_2401_16378_b200", "csrc", "build", "pd_k2c.o")
 CSEG_OBJ = os.path.join(ROOT, "paper_2401_16378_b200", "csrc", "build", "pd_k2cseg.o")
+Q_OBJ = os.path.join(ROOT, "paper_2401_16378_b200", "csrc", "build", "pd_k2q.o")
 WHT_OBJ = os.path.join(ROOT, "paper_2401_16378_b200", "csrc", "build", "pd_wht.o")
 CUOBJDUMP = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
 
@@ -80,13 +81,13 @@ def test_k2_streams_diagonals_with_bulk_copies():
 
 
 def test_no_local_memory_in_hot_kernels():
-    for obj in (OBJ, WHT_OBJ, SHARE_OBJ, C_OBJ, CSEG_OBJ):
+    for obj in (OBJ, WHT_OBJ, SHARE_OBJ, C_OBJ, CSEG_OBJ, Q_OBJ):
         log = open(obj + ".ptxas.log").read()
         for m in re.finditer(r"Function properties for (\S+)\n\s*(\d+) bytes stack frame, (\d+) bytes spill stores",
                              log):
             name, stack, spills = m.group(1), int(m.group(2)), int(m.group(3))
             if "gray_" in name or "wht_" in name or "diag_gather" in name:
-                assert spills == 0, (name, spills)
+                assert spills == 0 and stack == 0, (name, stack, spills)
 
 
 def test_k2_segment_instantiation_is_separate_and_clean():
