@@ -45,7 +45,7 @@ __device__ __forceinline__ void q_block(const double2* __restrict__ blk, unsigne
                                         QAcc<Q>& a) {
     constexpr int kQB = Q == 4 ? 2 : (Q == 2 ? 1 : 0);  // log2 Q
     unsigned cur = sgn;
-    if (ODD && kQB <= 3) cur ^= w[3];
+    if (ODD) cur ^= w[3];  // index bit 3 is set in odd blocks (always a thread bit: log2 Q <= 2)
 #pragma unroll
     for (int p = 0; p < 16; ++p) {
         const int il = static_cast<int>(cgray(p)) ^ (ODD ? 8 : 0);
