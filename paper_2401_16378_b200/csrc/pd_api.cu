@@ -106,7 +106,7 @@ struct pd_ctx {
     cudaStream_t h2d = nullptr;      // column-segment upload, overlapped with K2 segments
     cudaStream_t gather = nullptr;   // K1 on each uploaded segment (high priority: its CTAs are
                                      // dispatched ahead of the K2 walk's pending ones)
-    static constexpr int kBlocks = 32;  // >= 2^(download block bits)
+    static constexpr int kBlocks = 48;  // >= 2^(download block bits) - 1 + tail sub-blocks
     static constexpr int kSegs = 40;    // walk segments
     cudaEvent_t gathered = nullptr;
     cudaEvent_t block_done[kBlocks] = {};
@@ -599,7 +599,8 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
     //    so the result is bit-identical to one launch. Otherwise G goes up in one copy.
     //  * Download. The coefficients come back in 32 X-mask blocks; block q's (32 runs of
     //    4^(N-5), pd_run_offset) are copied while later blocks compute, so only the last
-    //    block's D2H is exposed.
+    //    block's D2H is exposed; at N >= 14 the last block runs as 4 sub-blocks, so only a
+    //    quarter of it is.
     double* dout = static_cast<double*>(ctx->out);
     double* diag = static_cast<double*>(ctx->scratch);
     double* gdev = static_cast<double*>(ctx->g);
@@ -610,19 +611,25 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
     constexpr unsigned kChunkLog = 10;  // 9 and 11 measured 500.5 and 508 ms (N=14 e2e)
     const unsigned nch = gray && pdb::gray_xmask_chunks(N) > 1 ? (1u << (N - kChunkLog)) : 1;
     const unsigned segs = nch >= pd_ctx::kSegs ? pd_ctx::kSegs : nch;
+    constexpr unsigned kTailLog = 2;  // last download block split in 4 (PD_E2E_TAIL)
     constexpr unsigned kBits = 5;  // 32 download blocks (N=14 e2e: 8 -> 540, 16 -> 520.4, 32 -> 518.1 ms)
     const uint64_t xc = dim >> kBits;
-    const uint64_t run = 1ull << (2 * (N - kBits));
     const unsigned nblk = 1u << kBits;
-    auto download = [&](unsigned q, cudaStream_t s) -> int {  // block q's runs, once computed
-        PD_CUDA(cudaEventRecord(ctx->block_done[q], s));
-        PD_CUDA(cudaStreamWaitEvent(ctx->d2h, ctx->block_done[q], 0));
-        for (unsigned r = 0; out && r < nblk; ++r) {
-            const uint64_t off = 2 * pd_run_offset(N, kBits, q, r);
-            PD_CUDA(cudaMemcpyAsync(out + off, dout + off, run * sizeof(double2),
+    // the coefficients of the X-masks whose top `bits` bits equal xt: 2^bits runs of
+    // 4^(N - bits), one per value of z's top bits (pd_run_offset); event slot ev
+    auto download_bits = [&](unsigned bits, uint64_t xt, unsigned ev, cudaStream_t s) -> int {
+        PD_CUDA(cudaEventRecord(ctx->block_done[ev], s));
+        PD_CUDA(cudaStreamWaitEvent(ctx->d2h, ctx->block_done[ev], 0));
+        const uint64_t len = 1ull << (2 * (N - bits));
+        for (uint64_t r = 0; out && r < (1ull << bits); ++r) {
+            const uint64_t off = 2 * pd_run_offset(N, bits, xt, r);
+            PD_CUDA(cudaMemcpyAsync(out + off, dout + off, len * sizeof(double2),
                                     cudaMemcpyDeviceToHost, ctx->d2h));
         }
         return PD_OK;
+    };
+    auto download = [&](unsigned q, cudaStream_t s) -> int {  // block q's runs, once computed
+        return download_bits(kBits, q, q, s);
     };
     // the walk segments keep raw partial sums of every coefficient (one more G-sized buffer);
     // without room for them, upload G whole and walk in one launch per download block
@@ -648,6 +655,9 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
         // so that the walk follows the upload instead of idling until a long segment's columns
         // have arrived (N=14 e2e, PR-1 split: doubling segments 1, 1, 2, 4, 8 510-515 ms; 4 x 1
         // then runs of 2: 500.5 ms)
+        // (walking the first chunk in 2 or 4 pieces so that it starts after 1/32 or 1/64 of G:
+        // 354.1 / 354.2 ms, no gain: from the third segment on the walk, not the upload, paces
+        // the first half)
         constexpr unsigned ones = 4, runlen = 2;
         unsigned bnd[pd_ctx::kSegs + 1];
         unsigned nb = 0;
@@ -695,16 +705,31 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
         PD_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->cols_ready[nseg - 1], 0));
         PD_CUDA(cudaEventRecord(ctx->seg_done, ctx->stream));
         PD_CUDA(cudaStreamWaitEvent(ctx->stream2, ctx->seg_done, 0));
+        // the last block runs as 2^tail_log sub-blocks so that only the last sub-block's
+        // download is exposed after the walk ends (N=14 e2e, PD_E2E_TAIL=0/1/2/3: 355.6 / 354.6 /
+        // 354.1 / 357.6 ms; smaller sub-blocks lose more to their partial last wave)
+        static const char* tail_env = std::getenv("PD_E2E_TAIL");
+        unsigned tail_log = tail_env ? static_cast<unsigned>(std::atoi(tail_env)) : kTailLog;
+        while (tail_log && (xc >> tail_log) < 128) --tail_log;
+        if (!tail_env && xc < 512) tail_log = 0;  // N=13 (256-X-mask blocks): 52.5 -> 54.0 ms split
+        if (nblk - 1 + (1u << tail_log) > static_cast<unsigned>(pd_ctx::kBlocks)) tail_log = 0;
+        unsigned launches = 0;
         for (unsigned q = 0; q < nblk; ++q) {
-            cudaStream_t s = (q & 1) ? ctx->stream2 : ctx->stream;
-            cudaError_t e = pdb::launch_gray_segment(
-                reinterpret_cast<const double2*>(diag) + q * xc * dim, N, q * xc, xc, bnd[nseg - 1], 0,
-                part + q * xc * dim, nullptr, 0, reinterpret_cast<double2*>(dout), PD_LAYOUT_GLOBAL,
-                s, kChunkLog);
-            if (e != cudaSuccess) return cuda_fail(e, "gray block launch");
-            tl.mark("blk" + std::to_string(q), s);
-            if (int rc = download(q, s)) return rc;
-            tl.mark("d2h" + std::to_string(q), ctx->d2h);
+            const unsigned sub_log = q + 1 == nblk ? tail_log : 0;
+            const uint64_t xs = xc >> sub_log;
+            for (uint64_t sb = 0; sb < (1ull << sub_log); ++sb, ++launches) {
+                cudaStream_t s = (launches & 1) ? ctx->stream2 : ctx->stream;
+                const uint64_t x0 = q * xc + sb * xs;
+                cudaError_t e = pdb::launch_gray_segment(
+                    reinterpret_cast<const double2*>(diag) + x0 * dim, N, x0, xs, bnd[nseg - 1], 0,
+                    part + x0 * dim, nullptr, 0, reinterpret_cast<double2*>(dout), PD_LAYOUT_GLOBAL,
+                    s, kChunkLog);
+                if (e != cudaSuccess) return cuda_fail(e, "gray block launch");
+                tl.mark("blk" + std::to_string(launches), s);
+                if (int rc = download_bits(kBits + sub_log, (uint64_t{q} << sub_log) | sb, launches, s))
+                    return rc;
+                tl.mark("d2h" + std::to_string(launches), ctx->d2h);
+            }
         }
     } else {
         if (int rc = upload(ctx, ctx->g, g, bytes)) return rc;
