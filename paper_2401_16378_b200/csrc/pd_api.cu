@@ -732,12 +732,33 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
             }
         }
     } else {
-        if (int rc = upload(ctx, ctx->g, g, bytes)) return rc;
-        if (gray && pd_diag_gather_device(N, gdev, 0, dim, diag, ctx->stream)) return PD_ECUDA;
-        PD_CUDA(cudaEventRecord(ctx->gathered, ctx->stream));
-        PD_CUDA(cudaStreamWaitEvent(ctx->stream2, ctx->gathered, 0));
+        // WHT: block q's X-masks (top kBits bits = q) read only the tiles (t ^ q, t) of G, so G
+        // goes up tile-wise per block on the copy stream and block q transforms as soon as its
+        // 1/32 of G has arrived; earlier blocks' downloads overlap later blocks' uploads
+        // (PCIe is full duplex), instead of the whole upload, then the whole download
+        static const char* tiled_env = std::getenv("PD_E2E_WHT_TILED");
+        const bool tiled = !gray && nblk <= static_cast<unsigned>(pd_ctx::kSegs) &&
+                           !(tiled_env && tiled_env[0] == '0');
+        if (!tiled) {
+            if (int rc = upload(ctx, ctx->g, g, bytes)) return rc;
+            if (gray && pd_diag_gather_device(N, gdev, 0, dim, diag, ctx->stream)) return PD_ECUDA;
+            PD_CUDA(cudaEventRecord(ctx->gathered, ctx->stream));
+            PD_CUDA(cudaStreamWaitEvent(ctx->stream2, ctx->gathered, 0));
+        }
+        tl.mark("start", tiled ? ctx->h2d : ctx->stream);
         for (unsigned q = 0; q < nblk; ++q) {
             cudaStream_t s = (q & 1) ? ctx->stream2 : ctx->stream;
+            if (tiled) {
+                for (uint64_t t = 0; t < nblk; ++t) {
+                    const uint64_t off = 2 * (((t ^ q) * xc) * dim + t * xc);  // tile (t ^ q, t)
+                    PD_CUDA(cudaMemcpy2DAsync(gdev + off, dim * sizeof(double2), g + off,
+                                              dim * sizeof(double2), xc * sizeof(double2), xc,
+                                              cudaMemcpyHostToDevice, ctx->h2d));
+                }
+                PD_CUDA(cudaEventRecord(ctx->copied[q], ctx->h2d));
+                tl.mark("up" + std::to_string(q), ctx->h2d);
+                PD_CUDA(cudaStreamWaitEvent(s, ctx->copied[q], 0));
+            }
             int rc;
             if (gray) {
                 cudaError_t e = pdb::launch_gray_segment(

@@ -119,16 +119,19 @@ def test_wht_fused_sizes(pd, cuda, port, nq):
     assert same_values(pd.decompose(g)[ns.astype(np.int64)], port.coeff_batch(g, ns))
 
 
-@pytest.mark.parametrize("nq", [12, 13])
-def test_host_pipeline_matches_device_path(pd, cuda, nq):
+@pytest.mark.parametrize("path", ["gray", "wht"])
+@pytest.mark.parametrize("nq", [10, 12, 13])
+def test_host_pipeline_matches_device_path(pd, cuda, nq, path):
+    # the host pipelines (Gray: column segments; WHT: per-block tile uploads) against one
+    # device-resident decomposition of the same matrix
     import torch
     g = normal_matrix(np.random.default_rng(1300 + nq), nq)
     gd = torch.from_numpy(g).to(cuda)
     out = torch.empty(4**nq, dtype=torch.complex128, device=cuda)
     scratch = torch.empty(4**nq, dtype=torch.complex128, device=cuda)
-    pd.device.decompose(nq, gd.data_ptr(), out.data_ptr(), scratch.data_ptr(), "gray", 0)
+    pd.device.decompose(nq, gd.data_ptr(), out.data_ptr(), scratch.data_ptr(), path, 0)
     torch.cuda.synchronize()
-    assert np.array_equal(pd.decompose(g), out.cpu().numpy())
+    assert np.array_equal(pd.decompose(g, path=path), out.cpu().numpy())
 
 
 def test_integer_inputs_bit_exact_any_order(pd, cuda, port):
