@@ -611,6 +611,7 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
     constexpr unsigned kChunkLog = 10;  // 9 and 11 measured 500.5 and 508 ms (N=14 e2e)
     const unsigned nch = gray && pdb::gray_xmask_chunks(N) > 1 ? (1u << (N - kChunkLog)) : 1;
     const unsigned segs = nch >= pd_ctx::kSegs ? pd_ctx::kSegs : nch;
+    constexpr unsigned kWhtGroupLog = 1;  // WHT host path: blocks per tile upload (log2)
     constexpr unsigned kTailLog = 2;  // last download block split in 4 (PD_E2E_TAIL)
     constexpr unsigned kBits = 5;  // 32 download blocks (N=14 e2e: 8 -> 540, 16 -> 520.4, 32 -> 518.1 ms)
     const uint64_t xc = dim >> kBits;
@@ -739,6 +740,9 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
         static const char* tiled_env = std::getenv("PD_E2E_WHT_TILED");
         const bool tiled = !gray && nblk <= static_cast<unsigned>(pd_ctx::kSegs) &&
                            !(tiled_env && tiled_env[0] == '0');
+        static const char* grp_env = std::getenv("PD_E2E_WHT_GROUP");
+        unsigned wht_grp = grp_env ? static_cast<unsigned>(std::atoi(grp_env)) : kWhtGroupLog;
+        if (wht_grp > kBits) wht_grp = kBits;
         if (!tiled) {
             if (int rc = upload(ctx, ctx->g, g, bytes)) return rc;
             if (gray && pd_diag_gather_device(N, gdev, 0, dim, diag, ctx->stream)) return PD_ECUDA;
@@ -749,15 +753,22 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
         for (unsigned q = 0; q < nblk; ++q) {
             cudaStream_t s = (q & 1) ? ctx->stream2 : ctx->stream;
             if (tiled) {
-                for (uint64_t t = 0; t < nblk; ++t) {
-                    const uint64_t off = 2 * (((t ^ q) * xc) * dim + t * xc);  // tile (t ^ q, t)
-                    PD_CUDA(cudaMemcpy2DAsync(gdev + off, dim * sizeof(double2), g + off,
-                                              dim * sizeof(double2), xc * sizeof(double2), xc,
-                                              cudaMemcpyHostToDevice, ctx->h2d));
+                // blocks go up in groups of 2^grp: for row block r the group's tiles are the
+                // aligned run of 2^grp column blocks holding r ^ q, one wider copy per row block
+                // (N=14 e2e, PD_E2E_WHT_GROUP=0/1/2/3, 8-64 KiB rows: 111.0 / 102.7 / 109.2 / 116.5 ms)
+                const uint64_t gw = 1ull << wht_grp;
+                if ((q & (gw - 1)) == 0) {
+                    for (uint64_t r = 0; r < nblk; ++r) {
+                        const uint64_t c0 = (r ^ q) & ~(gw - 1);
+                        const uint64_t off = 2 * ((r * xc) * dim + c0 * xc);
+                        PD_CUDA(cudaMemcpy2DAsync(gdev + off, dim * sizeof(double2), g + off,
+                                                  dim * sizeof(double2), gw * xc * sizeof(double2), xc,
+                                                  cudaMemcpyHostToDevice, ctx->h2d));
+                    }
+                    PD_CUDA(cudaEventRecord(ctx->copied[q], ctx->h2d));
+                    tl.mark("up" + std::to_string(q), ctx->h2d);
                 }
-                PD_CUDA(cudaEventRecord(ctx->copied[q], ctx->h2d));
-                tl.mark("up" + std::to_string(q), ctx->h2d);
-                PD_CUDA(cudaStreamWaitEvent(s, ctx->copied[q], 0));
+                PD_CUDA(cudaStreamWaitEvent(s, ctx->copied[q & ~(gw - 1)], 0));
             }
             int rc;
             if (gray) {
