@@ -244,7 +244,8 @@ def run_ours(args) -> None:
     pd_seed = pd.matrix_seed(ACCEPT_SEED, nq, 0)  # the reference generator's seed (bench.cpp:42-46)
     if rank == 0:
         pd.device.random_matrix(nq, pd_seed, G.data_ptr(), sptr)
-    diag = torch.empty(plan.x_count * dim, dtype=torch.complex128, device=dev)
+    from paper_2401_16378_b200.sharding import scratch_tensor
+    diag = scratch_tensor(nq, plan.x_count, args.path, dev)  # diagonals + non-finite flags
     out = torch.empty(4**nq, dtype=torch.complex128, device=dev) if rank == 0 else None
     peer = args.mode == "peer" and world > 1
     local = None if rank == 0 or peer else torch.empty(plan.run_len << plan.run_bits,

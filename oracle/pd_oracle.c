@@ -17,6 +17,7 @@
  * Every function cites the reference file:line it restates (paths relative to
  * the reference's proj/ directory).
  */
+#include <math.h>
 #include <pthread.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -51,10 +52,71 @@ PDO_EXPORT uint64_t pdo_gray_code(uint64_t k) { return k ^ (k >> 1); }
 PDO_EXPORT unsigned pdo_flipped_bit_index(uint64_t k) { return (unsigned)__builtin_ctzll(k + 1); }
 
 /*
+ * The reference's term is lambda.value() * a[...] (decompose.cpp:40): a
+ * std::complex<double> product, which GCC evaluates as (ac - bd, ad + bc) and,
+ * when both parts are NaN, passes to libgcc's __muldc3 — the infinity recovery
+ * of C99 Annex G.5.1, restated here. lambda = unit_phase(p) (pauli.hpp:71-76).
+ */
+static void cmul_annex_g(double a, double b, double c, double d, double* re, double* im) {
+    const double ac = a * c, bd = b * d, ad = a * d, bc = b * c;
+    double x = ac - bd, y = ad + bc;
+    if (isnan(x) && isnan(y)) {
+        int recalc = 0;
+        if (isinf(a) || isinf(b)) { /* first factor infinite: box it, the other's NaNs -> 0 */
+            a = copysign(isinf(a) ? 1.0 : 0.0, a);
+            b = copysign(isinf(b) ? 1.0 : 0.0, b);
+            if (isnan(c)) c = copysign(0.0, c);
+            if (isnan(d)) d = copysign(0.0, d);
+            recalc = 1;
+        }
+        if (isinf(c) || isinf(d)) { /* second factor infinite */
+            c = copysign(isinf(c) ? 1.0 : 0.0, c);
+            d = copysign(isinf(d) ? 1.0 : 0.0, d);
+            if (isnan(a)) a = copysign(0.0, a);
+            if (isnan(b)) b = copysign(0.0, b);
+            recalc = 1;
+        }
+        if (!recalc && (isinf(ac) || isinf(bd) || isinf(ad) || isinf(bc))) { /* overflow */
+            if (isnan(a)) a = copysign(0.0, a);
+            if (isnan(b)) b = copysign(0.0, b);
+            if (isnan(c)) c = copysign(0.0, c);
+            if (isnan(d)) d = copysign(0.0, d);
+            recalc = 1;
+        }
+        if (recalc) {
+            x = INFINITY * (a * c - b * d);
+            y = INFINITY * (a * d + b * c);
+        }
+    }
+    *re = x;
+    *im = y;
+}
+
+static const double kUnitRe[4] = {1.0, 0.0, -1.0, 0.0}; /* pauli.hpp:71-76 unit_phase */
+static const double kUnitIm[4] = {0.0, 1.0, 0.0, -1.0};
+
+/* acc += i^lam · (er + i ei). For a finite element the product is the exact re/im swap with
+ * sign (the reference's product up to the sign of an exact zero); an infinite or NaN element
+ * takes the reference's full complex product, whose 0·inf terms are NaN. */
+static inline void add_term(unsigned lam, double er, double ei, double* ar, double* ai) {
+    if (!(isfinite(er) && isfinite(ei))) {
+        double tr, ti;
+        cmul_annex_g(kUnitRe[lam], kUnitIm[lam], er, ei, &tr, &ti);
+        *ar += tr;
+        *ai += ti;
+        return;
+    }
+    switch (lam) { /* i^lam · (er + i ei) */
+        case 0: *ar += er; *ai += ei; break;
+        case 1: *ar += -ei; *ai += er; break;
+        case 2: *ar += -er; *ai += -ei; break;
+        default: *ar += ei; *ai += -er; break;
+    }
+}
+
+/*
  * decompose.cpp:30-47 gray_walk_sum + :49-57 coeff_fast_impl.
- * λ is a 2-bit power of i (pauli.hpp:91-125); λ·a for λ ∈ {1,i,-1,-i} is an
- * exact re/im swap with sign, identical to the reference's complex product
- * except possibly for the sign of an exact zero term. The walk visits
+ * λ is a 2-bit power of i (pauli.hpp:91-125); λ·a is add_term above. The walk visits
  * i = gray(k) for k = 0..dim-1 and after each step multiplies λ by the row-flip
  * quotient of the digit at the flipped bit: -1 for Y and Z (pauli.hpp:66-68).
  */
@@ -66,13 +128,7 @@ static void coeff_fast_raw(unsigned N, const double* g, uint64_t n, double* out)
     uint64_t code = 0;
     for (uint64_t step = 0;; ++step) {
         const double* e = g + 2 * ((code ^ mask) * dim + code);
-        const double er = e[0], ei = e[1];
-        switch (lam) { /* i^lam · (er + i ei) */
-            case 0: ar += er; ai += ei; break;
-            case 1: ar += -ei; ai += er; break;
-            case 2: ar += -er; ai += -ei; break;
-            default: ar += ei; ai += -er; break;
-        }
+        add_term(lam, e[0], e[1], &ar, &ai);
         if (step + 1 == dim) break;
         const unsigned t = (unsigned)__builtin_ctzll(step + 1);
         lam = (lam + ((digit(n, t) >> 1) ? 2u : 0u)) & 3u;
@@ -104,12 +160,7 @@ PDO_EXPORT int pdo_coeff_slow(unsigned N, const double* g, uint64_t n, double* o
         unsigned lam = 0;
         for (unsigned t = 0; t < N; ++t) lam += beta[digit(n, t)][(i >> t) & 1u];
         const double* e = g + 2 * ((i ^ mask) * dim + i);
-        switch (lam & 3u) {
-            case 0: ar += e[0]; ai += e[1]; break;
-            case 1: ar += -e[1]; ai += e[0]; break;
-            case 2: ar += -e[0]; ai += -e[1]; break;
-            default: ar += e[1]; ai += -e[0]; break;
-        }
+        add_term(lam & 3u, e[0], e[1], &ar, &ai);
     }
     out[0] = ar / (double)dim;
     out[1] = ai / (double)dim;
@@ -186,12 +237,7 @@ PDO_EXPORT int pdo_recompose(unsigned N, const double* coeffs, double* out) {
         uint64_t code = 0;
         for (uint64_t step = 0;; ++step) {
             double* a = out + 2 * (code * dim + (code ^ mask));
-            switch (lam) {
-                case 0: a[0] += cr; a[1] += ci; break;
-                case 1: a[0] += -ci; a[1] += cr; break;
-                case 2: a[0] += -cr; a[1] += -ci; break;
-                default: a[0] += ci; a[1] += -cr; break;
-            }
+            add_term(lam, cr, ci, &a[0], &a[1]);
             if (step + 1 == dim) break;
             const unsigned t = (unsigned)__builtin_ctzll(step + 1);
             lam = (lam + ((digit(n, t) >> 1) ? 2u : 0u)) & 3u;

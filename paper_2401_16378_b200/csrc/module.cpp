@@ -44,8 +44,9 @@ Path parse_path(const std::string& s) {
 py::array_t<Complex> py_decompose(const ComplexArray& g, unsigned threads, bool serial,
                                   const std::string& path, py::object out, py::object devices) {
     const unsigned N = matrix_qubits(g);
-    if (threads == 0) throw std::invalid_argument("thread count must be at least 1");
-    (void)serial;  // the quaternary driver yields the same coefficients (decompose.cpp:133-152)
+    // the serial quaternary driver ignores `threads`; the parallel one rejects 0
+    // (module.cpp:56-60 -> decompose.cpp:98-99, 133-152); both yield the same coefficients
+    if (!serial && threads == 0) throw std::invalid_argument("thread count must be at least 1");
     const Path p = parse_path(path);
     const py::ssize_t count = static_cast<py::ssize_t>(1) << (2 * N);
     py::array_t<Complex> result;

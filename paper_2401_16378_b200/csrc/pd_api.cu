@@ -309,7 +309,13 @@ int pd_xmask_coeffs_device(unsigned N, const double* diag, uint64_t x0, uint64_t
     double2* o = reinterpret_cast<double2*>(out);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     switch (path) {
-        case PD_PATH_GRAY: e = pdb::launch_gray_xmask(d, N, x0, x_count, run_bits, o, layout, s); break;
+        case PD_PATH_GRAY:
+            e = pdb::launch_gray_xmask(d, N, x0, x_count, run_bits, o, layout, s);
+            // X-masks with an inf or NaN on their diagonal: the reference's complex products
+            if (e == cudaSuccess)
+                e = pdb::launch_nonfinite_fixup(d, false, N, x0, x_count,
+                                                pdb::make_outmap(o, N, run_bits, layout), nullptr, s);
+            break;
         case PD_PATH_WHT:
             if (N > 16) return fail(PD_EINVAL, "the WHT path supports N <= 16");
             e = pdb::launch_wht_xmask(d, N, x0, x_count, run_bits, o, layout, s);
@@ -504,13 +510,13 @@ int pd_first_nonfinite_device(const double* g, uint64_t count, uint64_t* first, 
     if (int rc = check_device()) return rc;
     if (!first) return fail(PD_EINVAL, "null output");
     unsigned long long* d = nullptr;
-    PD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(*d), static_cast<cudaStream_t>(stream)));
+    PD_CUDA(pdb::pool_alloc(reinterpret_cast<void**>(&d), sizeof(*d), static_cast<cudaStream_t>(stream)));
     cudaError_t e = pdb::launch_first_nonfinite(reinterpret_cast<const double2*>(g), count, d,
                                                 static_cast<cudaStream_t>(stream));
     unsigned long long h = ~0ull;
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, static_cast<cudaStream_t>(stream));
-    cudaFreeAsync(d, static_cast<cudaStream_t>(stream));
+    pdb::pool_free(d, static_cast<cudaStream_t>(stream));
     if (e == cudaSuccess) e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "first_nonfinite");
     *first = h;
@@ -604,6 +610,9 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
     double* dout = static_cast<double*>(ctx->out);
     double* diag = static_cast<double*>(ctx->scratch);
     double* gdev = static_cast<double*>(ctx->g);
+    // a block's X-masks whose diagonal holds an inf or NaN get the reference's products
+    // (pd_nonfinite.cu) before their download
+    const pdb::OutMap gmap = pdb::make_outmap(reinterpret_cast<double2*>(dout), N, 0, PD_LAYOUT_GLOBAL);
     const bool gray = path == PD_PATH_GRAY;
     HostTimeline tl;
     // the host pipeline walks in chunks of 1024 columns (half K2's default) so that the first,
@@ -725,6 +734,9 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
                     reinterpret_cast<const double2*>(diag) + x0 * dim, N, x0, xs, bnd[nseg - 1], 0,
                     part + x0 * dim, nullptr, 0, reinterpret_cast<double2*>(dout), PD_LAYOUT_GLOBAL,
                     s, kChunkLog);
+                if (e == cudaSuccess)
+                    e = pdb::launch_nonfinite_fixup(reinterpret_cast<const double2*>(diag) + x0 * dim,
+                                                    false, N, x0, xs, gmap, nullptr, s);
                 if (e != cudaSuccess) return cuda_fail(e, "gray block launch");
                 tl.mark("blk" + std::to_string(launches), s);
                 if (int rc = download_bits(kBits + sub_log, (uint64_t{q} << sub_log) | sb, launches, s))
@@ -772,9 +784,12 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
             }
             int rc;
             if (gray) {
-                cudaError_t e = pdb::launch_gray_segment(
-                    reinterpret_cast<const double2*>(diag) + q * xc * dim, N, q * xc, xc, 0, 0, nullptr,
-                    nullptr, 0, reinterpret_cast<double2*>(dout), PD_LAYOUT_GLOBAL, s);
+                const double2* dq = reinterpret_cast<const double2*>(diag) + q * xc * dim;
+                cudaError_t e = pdb::launch_gray_segment(dq, N, q * xc, xc, 0, 0, nullptr, nullptr, 0,
+                                                         reinterpret_cast<double2*>(dout),
+                                                         PD_LAYOUT_GLOBAL, s);
+                if (e == cudaSuccess)
+                    e = pdb::launch_nonfinite_fixup(dq, false, N, q * xc, xc, gmap, nullptr, s);
                 rc = e == cudaSuccess ? PD_OK : cuda_fail(e, "gray block launch");
             } else {
                 // WHT: each block gathers and transforms its own X-masks from G (fused two-pass)

@@ -10,6 +10,8 @@
 //     (pauli.hpp:97-102) and row-flip quotient -1 for Y,Z (pauli.hpp:65-68).
 #pragma once
 
+#include <math_constants.h>
+
 #include <cstdint>
 
 namespace pdb {
@@ -80,6 +82,85 @@ __device__ __forceinline__ double2 apply_phase(unsigned p, double sr, double si,
         default: cr = si; ci = -sr; break;
     }
     return make_double2(cr * scale, ci * scale);
+}
+
+// ---- the reference's own arithmetic, for non-finite elements ----
+//
+// The reference accumulates lambda.value() * a[...] (decompose.cpp:40), a std::complex<double>
+// product that GCC evaluates as (ac - bd, ad + bc) and, when both parts come out NaN, hands to
+// libgcc's __muldc3, which recovers infinities as C99 Annex G.5.1 specifies. For lambda in
+// {1, i, -1, -i} and a finite element that is the exact re/im swap the fast kernels fold into
+// their adds (up to the sign of an exact zero); for an infinite or NaN element it is not:
+// 0 * inf puts a NaN into the other component ([[1, inf], [3, 4]] -> c_1 = inf + nan i).
+// Products are rounded one by one (no contraction), as the reference's x86-64 SSE code does.
+
+__device__ __forceinline__ bool finite2(double2 v) {
+    return ((__double2hiint(v.x) & 0x7ff00000) != 0x7ff00000) &
+           ((__double2hiint(v.y) & 0x7ff00000) != 0x7ff00000);
+}
+
+__device__ __forceinline__ double2 cmul_annex_g(double a, double b, double c, double d) {
+    const double ac = __dmul_rn(a, c), bd = __dmul_rn(b, d), ad = __dmul_rn(a, d),
+                 bc = __dmul_rn(b, c);
+    double x = __dsub_rn(ac, bd), y = __dadd_rn(ad, bc);
+    if (isnan(x) && isnan(y)) {
+        bool recalc = false;
+        if (isinf(a) || isinf(b)) {  // the first factor is infinite: box it, NaNs of the other -> 0
+            a = copysign(isinf(a) ? 1.0 : 0.0, a);
+            b = copysign(isinf(b) ? 1.0 : 0.0, b);
+            if (isnan(c)) c = copysign(0.0, c);
+            if (isnan(d)) d = copysign(0.0, d);
+            recalc = true;
+        }
+        if (isinf(c) || isinf(d)) {  // the second factor is infinite
+            c = copysign(isinf(c) ? 1.0 : 0.0, c);
+            d = copysign(isinf(d) ? 1.0 : 0.0, d);
+            if (isnan(a)) a = copysign(0.0, a);
+            if (isnan(b)) b = copysign(0.0, b);
+            recalc = true;
+        }
+        if (!recalc && (isinf(ac) || isinf(bd) || isinf(ad) || isinf(bc))) {  // overflow
+            if (isnan(a)) a = copysign(0.0, a);
+            if (isnan(b)) b = copysign(0.0, b);
+            if (isnan(c)) c = copysign(0.0, c);
+            if (isnan(d)) d = copysign(0.0, d);
+            recalc = true;
+        }
+        if (recalc) {
+            x = __dmul_rn(CUDART_INF, __dsub_rn(__dmul_rn(a, c), __dmul_rn(b, d)));
+            y = __dmul_rn(CUDART_INF, __dadd_rn(__dmul_rn(a, d), __dmul_rn(b, c)));
+        }
+    }
+    return make_double2(x, y);
+}
+
+// i^p as the reference's unit_phase table (pauli.hpp:71-76)
+__device__ __forceinline__ double unit_re(unsigned p) { return p == 0 ? 1.0 : (p == 2 ? -1.0 : 0.0); }
+__device__ __forceinline__ double unit_im(unsigned p) { return p == 1 ? 1.0 : (p == 3 ? -1.0 : 0.0); }
+
+// Coefficient (x, z) by the reference's arithmetic: k = 0..2^N-1 in Gray order, lambda carried as
+// a power of i from (-i)^{|x&z|} (pauli.hpp:97-102) and multiplied by -1 when the flipped bit is
+// set in z (pauli.hpp:65-68, 112-114), acc += lambda * e with cmul_annex_g, then acc / 2^N
+// componentwise (complex / double, decompose.cpp:56). elem(i) returns G[i ^ x][i].
+template <class Elem>
+__device__ __forceinline__ double2 exact_coeff(const Elem& elem, unsigned N, uint64_t x, uint64_t z) {
+    const uint64_t dim = 1ull << N;
+    unsigned p = (3u * static_cast<unsigned>(__popcll(x & z))) & 3u;
+    double ar = 0.0, ai = 0.0;
+    uint64_t code = 0;
+    for (uint64_t k = 0;; ++k) {
+        const double2 e = elem(code);
+        const double2 t = cmul_annex_g(unit_re(p), unit_im(p), e.x, e.y);
+        ar = __dadd_rn(ar, t.x);
+        ai = __dadd_rn(ai, t.y);
+        if (k + 1 == dim) break;
+        const unsigned b = static_cast<unsigned>(__ffsll(static_cast<long long>(k + 1)) - 1);
+        p = (p + 2u * static_cast<unsigned>((z >> b) & 1u)) & 3u;
+        code ^= 1ull << b;
+    }
+    // acc / 2^N: the product with 2^-N is the same correctly rounded quotient (subnormals too)
+    const double s = __longlong_as_double(static_cast<long long>(1023 - N) << 52);
+    return make_double2(__dmul_rn(ar, s), __dmul_rn(ai, s));
 }
 
 // Where coefficient (x, z) with tensor number n goes (see pd_api.h, pd_layout):

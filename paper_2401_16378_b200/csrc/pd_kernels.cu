@@ -270,7 +270,14 @@ __global__ void __launch_bounds__(128)
         }
     }
     const unsigned ph = (3u * static_cast<unsigned>(__popcll(x & z))) & 3u;
-    out[k] = apply_phase(ph, sr, si, scale);
+    double2 c = apply_phase(ph, sr, si, scale);
+    if (!finite2(c)) {
+        // an inf or NaN on the diagonal (a finite one cannot make the sum non-finite without
+        // overflow, where both arithmetics agree): the reference's complex products instead
+        const auto elem = [=](uint64_t i) { return __ldg(&G[(i ^ x) * row_stride + i]); };
+        c = exact_coeff(elem, N, x, z);
+    }
+    out[k] = c;
 }
 
 // row_stride = 2^N walks G itself; row_stride = 0 walks a compact diagonal D[i] = G[i ^ x][i]
@@ -363,7 +370,12 @@ __global__ void __launch_bounds__(kW1Threads)
     }
     if (threadIdx.x == 0) {
         const unsigned ph = (3u * static_cast<unsigned>(__popcll(x & z))) & 3u;
-        *out = apply_phase(ph, sr, si, scale);
+        double2 c = apply_phase(ph, sr, si, scale);
+        if (!finite2(c)) {  // non-finite element: the reference's complex products (walk_kernel)
+            const auto elem = [=](uint64_t i) { return D[i]; };
+            c = exact_coeff(elem, N, x, z);
+        }
+        *out = c;
     }
 }
 
@@ -427,8 +439,9 @@ __global__ void kron_trace_kernel(const double2* __restrict__ G, unsigned N, uin
                 pi = ni;
             }
             const double2 g = G[j * dim + i];
-            tr += pr * g.x - pi * g.y;
-            ti += pr * g.y + pi * g.x;
+            const double2 t = cmul_annex_g(pr, pi, g.x, g.y);  // the reference's complex product
+            tr = __dadd_rn(tr, t.x);
+            ti = __dadd_rn(ti, t.y);
         }
     }
     out[0] = make_double2(tr / static_cast<double>(dim), ti / static_cast<double>(dim));

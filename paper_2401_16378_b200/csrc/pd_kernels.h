@@ -6,6 +6,8 @@
 #include <atomic>
 #include <cstdint>
 
+#include "pd_device.cuh"
+
 namespace pdb {
 
 constexpr unsigned kMaxRunBits = 8;  // run bits of the RUNS output layout (shards x sub-blocks)
@@ -19,6 +21,21 @@ cudaError_t launch_diag_gather(const double2* G, unsigned N, uint64_t x0, uint64
 // K1 restricted to the columns [col0, col0 + cols) (a power-of-two aligned range)
 cudaError_t launch_diag_gather_cols(const double2* G, unsigned N, uint64_t x0, uint64_t x_count,
                                     uint64_t col0, uint64_t cols, double2* diag, cudaStream_t stream);
+
+// Non-finite elements (pd_nonfinite.cu). After a fast kernel has stored the coefficients of the
+// X-masks [x0, x0 + x_count) through `map`, every X-mask whose Z-mask-0 coefficient (the plain
+// sum of its diagonal) is not finite gets all its coefficients recomputed with the reference's
+// complex products. src: the gathered diagonals (row x - x0), or G itself when from_matrix.
+// With `flags` (x_count words) the X-masks are the flagged ones instead (nonfinite_scan).
+cudaError_t launch_nonfinite_fixup(const double2* src, bool from_matrix, unsigned N, uint64_t x0,
+                                   uint64_t x_count, const OutMap& map, const unsigned* flags,
+                                   cudaStream_t stream);
+// flags[x - x0] = 1 if D_x (row x - x0 of diag) holds a non-finite element, else 0
+cudaError_t launch_nonfinite_scan(const double2* diag, unsigned N, uint64_t x_count, unsigned* flags,
+                                  cudaStream_t stream);
+// stream-ordered scratch from the library's own memory pool (not the device's default pool)
+cudaError_t pool_alloc(void** p, size_t bytes, cudaStream_t stream);
+cudaError_t pool_free(void* p, cudaStream_t stream);
 
 // K2 over the walk chunks [c_begin, c_end) (c_end = 0: to the end), continuing from raw sums
 // part_in (null: from zero) and storing raw sums to part_out (null: finished coefficients)

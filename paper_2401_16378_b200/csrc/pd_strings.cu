@@ -166,8 +166,13 @@ __device__ __forceinline__ void walk_bucket(unsigned N, const uint64_t* __restri
         for (int j = 0; j < kSwStr; ++j) {
             if (idx[j] == ~0u) continue;
             const unsigned ph = (3u * static_cast<unsigned>(__popcll(x & zs[j]))) & 3u;
-            out[idx[j]] = apply_phase(ph, flip_hi(st.sr[j], st.sig[j]), flip_hi(st.si[j], st.sig[j]),
-                                      scale);
+            double2 c = apply_phase(ph, flip_hi(st.sr[j], st.sig[j]), flip_hi(st.si[j], st.sig[j]),
+                                    scale);
+            if (!finite2(c)) {  // non-finite element: the reference's complex products
+                const auto elem = [=](uint64_t i) { return dx[i]; };
+                c = exact_coeff(elem, N, x, zs[j]);
+            }
+            out[idx[j]] = c;
         }
     }
 }
@@ -262,21 +267,12 @@ cudaError_t launch_strings_grouped(const double2* G, unsigned N, const uint64_t*
                                    uint64_t count, double2* out, cudaStream_t stream) {
     const unsigned nb = 1u << N;
     const size_t meta = (3ull * nb + 1) * sizeof(unsigned);
-    static std::atomic<uint64_t> pool_set{0};  // one bit per device
     int dev = 0;
     cudaGetDevice(&dev);
-    if (!(pool_set.load() >> dev & 1)) {
-        // keep freed blocks in the device's default pool: the per-call scratch then costs a
-        // pool lookup instead of a driver allocation (measured: 45 us of fixed cost otherwise)
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t keep = ~0ull;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-        }
-        pool_set.fetch_or(1ull << dev);
-    }
+    // per-call scratch from the library's own pool (pool_alloc, pd_nonfinite.cu), which keeps
+    // freed blocks: a pool lookup instead of a driver allocation (measured: 45 us otherwise)
     void* scratch = nullptr;
-    cudaError_t e = cudaMallocAsync(&scratch, meta + count * sizeof(unsigned), stream);
+    cudaError_t e = pool_alloc(&scratch, meta + count * sizeof(unsigned), stream);
     if (e != cudaSuccess) return e;
     unsigned* cnt = static_cast<unsigned*>(scratch);  // nb counts, nb cursors, nb + 1 offsets
     unsigned* cur = cnt + nb;
@@ -288,7 +284,7 @@ cudaError_t launch_strings_grouped(const double2* G, unsigned N, const uint64_t*
         e = cudaFuncSetAttribute(strings_walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(sizeof(double2) << 13));
         if (e != cudaSuccess) {
-            cudaFreeAsync(scratch, stream);
+            pool_free(scratch, stream);
             return e;
         }
         attr_set.fetch_or(1ull << dev);
@@ -326,7 +322,7 @@ cudaError_t launch_strings_grouped(const double2* G, unsigned N, const uint64_t*
             e = cudaGetLastError();
         }
     }
-    cudaError_t f = cudaFreeAsync(scratch, stream);
+    cudaError_t f = pool_free(scratch, stream);
     return e != cudaSuccess ? e : f;
 }
 

@@ -39,7 +39,7 @@ __device__ __forceinline__ void store_coeff(const OutMap& map, uint64_t x, uint6
 
 __global__ void __launch_bounds__(kWhtThreads)
     wht_rows_kernel(double2* __restrict__ diag, unsigned N, unsigned L, uint64_t x0,
-                    OutMap map, double scale, int final_pass) {
+                    OutMap map, double scale, int final_pass, const unsigned* __restrict__ skip) {
     // final_pass != 0: emit coefficients; otherwise write the transformed row back
     extern __shared__ __align__(16) double2 row[];
     const uint64_t dim = 1ull << N;
@@ -61,6 +61,7 @@ __global__ void __launch_bounds__(kWhtThreads)
         __syncthreads();
     }
     if (final_pass) {
+        if (skip && skip[xl]) return;  // non-finite diagonal: pd_nonfinite.cu wrote these
         const uint64_t x = x0 + xl;
         for (unsigned j = threadIdx.x; j < len; j += kWhtThreads)
             store_coeff(map, x, j, row[j].x, row[j].y, scale);
@@ -72,7 +73,8 @@ __global__ void __launch_bounds__(kWhtThreads)
 template <int R>  // R = N - L high bits
 __global__ void __launch_bounds__(kWhtThreads)
     wht_cols_kernel(double2* __restrict__ diag, unsigned N, unsigned L, uint64_t x0,
-                    uint64_t x_count, OutMap map, double scale, int emit) {
+                    uint64_t x_count, OutMap map, double scale, int emit,
+                    const unsigned* __restrict__ skip) {
     const uint64_t t = static_cast<uint64_t>(blockIdx.x) * kWhtThreads + threadIdx.x;
     const uint64_t cols = 1ull << L;
     if (t >= x_count * cols) return;
@@ -96,6 +98,7 @@ __global__ void __launch_bounds__(kWhtThreads)
         for (int r = 0; r < (1 << R); ++r) diag[xl * dim + (static_cast<uint64_t>(r) << L) + il] = v[r];
         return;
     }
+    if (skip && skip[xl]) return;  // non-finite diagonal: pd_nonfinite.cu wrote these
     const uint64_t x = x0 + xl;
 #pragma unroll
     for (int r = 0; r < (1 << R); ++r)
@@ -521,7 +524,7 @@ __global__ void __launch_bounds__(kWhtThreads, 2)
 // shared driver: rows pass, then (N > 12) the column pass; emit != 0 writes
 // coefficients through `runs`, emit == 0 leaves the transform in place in `buf`
 static cudaError_t wht_passes(double2* buf, unsigned N, uint64_t x0, uint64_t x_count,
-                              const OutMap& map, int emit, cudaStream_t stream) {
+                              const OutMap& map, int emit, const unsigned* skip, cudaStream_t stream) {
     const unsigned L = N < kWhtMaxL ? N : kWhtMaxL;
     const unsigned R = N - L;
     if (R > 4) return cudaErrorInvalidValue;  // N <= 16
@@ -537,16 +540,16 @@ static cudaError_t wht_passes(double2* buf, unsigned N, uint64_t x0, uint64_t x_
     }
     const uint64_t grid1 = x_count << R;
     wht_rows_kernel<<<static_cast<unsigned>(grid1), kWhtThreads, sizeof(double2) << L, stream>>>(
-        buf, N, L, x0, map, scale, emit && R == 0);
+        buf, N, L, x0, map, scale, emit && R == 0, skip);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || R == 0) return e;
     const unsigned grid2 = static_cast<unsigned>(((x_count << L) + kWhtThreads - 1) / kWhtThreads);
     switch (R) {
-        case 1: wht_cols_kernel<1><<<grid2, kWhtThreads, 0, stream>>>(buf, N, L, x0, x_count, map, scale, emit); break;
-        case 2: wht_cols_kernel<2><<<grid2, kWhtThreads, 0, stream>>>(buf, N, L, x0, x_count, map, scale, emit); break;
-        case 3: wht_cols_kernel<3><<<grid2, kWhtThreads, 0, stream>>>(buf, N, L, x0, x_count, map, scale, emit); break;
-        default: wht_cols_kernel<4><<<grid2, kWhtThreads, 0, stream>>>(buf, N, L, x0, x_count, map, scale, emit); break;
+        case 1: wht_cols_kernel<1><<<grid2, kWhtThreads, 0, stream>>>(buf, N, L, x0, x_count, map, scale, emit, skip); break;
+        case 2: wht_cols_kernel<2><<<grid2, kWhtThreads, 0, stream>>>(buf, N, L, x0, x_count, map, scale, emit, skip); break;
+        case 3: wht_cols_kernel<3><<<grid2, kWhtThreads, 0, stream>>>(buf, N, L, x0, x_count, map, scale, emit, skip); break;
+        default: wht_cols_kernel<4><<<grid2, kWhtThreads, 0, stream>>>(buf, N, L, x0, x_count, map, scale, emit, skip); break;
     }
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return cudaGetLastError();
@@ -554,9 +557,25 @@ static cudaError_t wht_passes(double2* buf, unsigned N, uint64_t x0, uint64_t x_
 
 cudaError_t launch_wht_xmask(const double2* diag_c, unsigned N, uint64_t x0, uint64_t x_count,
                              unsigned run_bits, double2* out, int layout, cudaStream_t stream) {
-    // the passes rewrite the diagonal rows in place (they are scratch owned by the caller)
-    return wht_passes(const_cast<double2*>(diag_c), N, x0, x_count,
-                      make_outmap(out, N, run_bits, layout), 1, stream);
+    const OutMap map = make_outmap(out, N, run_bits, layout);
+    double2* diag = const_cast<double2*>(diag_c);
+    if (N <= kWhtMaxL) {
+        // one rows pass reads the diagonals and emits: D is intact for the non-finite fixup
+        cudaError_t e = wht_passes(diag, N, x0, x_count, map, 1, nullptr, stream);
+        if (e == cudaSuccess) e = launch_nonfinite_fixup(diag_c, false, N, x0, x_count, map, nullptr, stream);
+        return e;
+    }
+    // N > 12: the rows pass rewrites the diagonals in place (they are scratch owned by the
+    // caller), so X-masks with a non-finite element are found and done first, from the
+    // untouched diagonals, and the passes skip them
+    unsigned* flags = nullptr;
+    cudaError_t e = pool_alloc(reinterpret_cast<void**>(&flags), x_count * sizeof(unsigned), stream);
+    if (e != cudaSuccess) return e;
+    e = launch_nonfinite_scan(diag_c, N, x_count, flags, stream);
+    if (e == cudaSuccess) e = launch_nonfinite_fixup(diag_c, false, N, x0, x_count, map, flags, stream);
+    if (e == cudaSuccess) e = wht_passes(diag, N, x0, x_count, map, 1, flags, stream);
+    const cudaError_t f = pool_free(flags, stream);
+    return e != cudaSuccess ? e : f;
 }
 
 // pass 2 dispatch: the register-round kernel for HB in [4, 8], the generic one otherwise
@@ -683,10 +702,8 @@ static cudaError_t wht_two_pass(const double2* G, unsigned N, uint64_t x0, uint6
     return cudaGetLastError();
 }
 
-cudaError_t launch_wht_from_matrix(const double2* G, unsigned N, uint64_t x0, uint64_t x_count,
-                                   double2* scratch, unsigned run_bits, double2* out, int layout,
-                                   cudaStream_t stream) {
-    const OutMap map = make_outmap(out, N, run_bits, layout);
+static cudaError_t wht_from_matrix(const double2* G, unsigned N, uint64_t x0, uint64_t x_count,
+                                   double2* scratch, const OutMap& map, cudaStream_t stream) {
     const uint64_t S = wht_chunk(N);
     const unsigned hb = N - kLoBits;
     const bool reg_pass2 = hb >= 4 && hb <= 8;
@@ -709,6 +726,16 @@ cudaError_t launch_wht_from_matrix(const double2* G, unsigned N, uint64_t x0, ui
         e = cudaEventRecord(p.join[k], p.side[k]);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, p.join[k], 0);
     }
+    return e;
+}
+
+cudaError_t launch_wht_from_matrix(const double2* G, unsigned N, uint64_t x0, uint64_t x_count,
+                                   double2* scratch, unsigned run_bits, double2* out, int layout,
+                                   cudaStream_t stream) {
+    const OutMap map = make_outmap(out, N, run_bits, layout);
+    cudaError_t e = wht_from_matrix(G, N, x0, x_count, scratch, map, stream);
+    // X-masks whose diagonal holds an inf or NaN: the reference's products, straight from G
+    if (e == cudaSuccess) e = launch_nonfinite_fixup(G, true, N, x0, x_count, map, nullptr, stream);
     return e;
 }
 
@@ -764,7 +791,7 @@ cudaError_t launch_wht_inverse(const double2* coeffs, unsigned N, double2* scrat
 }
 
 cudaError_t launch_wht_inplace(double2* rows, unsigned N, uint64_t x_count, cudaStream_t stream) {
-    return wht_passes(rows, N, 0, x_count, make_outmap(nullptr, N, 0, 0), 0, stream);
+    return wht_passes(rows, N, 0, x_count, make_outmap(nullptr, N, 0, 0), 0, nullptr, stream);
 }
 
 }  // namespace pdb

@@ -53,6 +53,13 @@ def run_offset(num_qubits: int, run_bits: int, shard: int, run: int) -> int:
     return int(_ext.device.run_offset(num_qubits, run_bits, shard, run))
 
 
+def scratch_tensor(num_qubits: int, x_count: int, path: str, device) -> torch.Tensor:
+    """Scratch of an X-mask block (pd_scratch_bytes: its diagonals plus their non-finite
+    flags) as a complex128 tensor."""
+    nbytes = int(_ext.device.scratch_bytes(num_qubits, x_count, path))
+    return torch.empty((nbytes + 15) // 16, dtype=torch.complex128, device=device)
+
+
 def _ptr(buf) -> int:
     return buf.data_ptr() if isinstance(buf, torch.Tensor) else int(buf)
 
@@ -132,8 +139,8 @@ class ShardedDecomposer:
         self.mapper = mapper or (CudaIpcMapper() if mode == "peer" else None)
         p = self.plan
         # buffers=False: the caller owns the scratch (diag) and, in NCCL mode, sets .local
-        self.diag = torch.empty(max(p.x_count, 32) << num_qubits, dtype=torch.complex128,
-                                device=device) if buffers and device.type == "cuda" else None
+        self.diag = scratch_tensor(num_qubits, max(p.x_count, 32), path, device) \
+            if buffers and device.type == "cuda" else None
         self.local = None
         if buffers and p.rank != 0 and mode == "nccl":
             self.local = torch.empty(p.run_len << p.run_bits, dtype=torch.complex128, device=device)

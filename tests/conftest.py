@@ -58,8 +58,25 @@ def normal_matrix(rng, nq):
     return rng.standard_normal((d, d)) + 1j * rng.standard_normal((d, d))
 
 
+def device_scratch(pd, nq, x_count=None, path="gray", device="cuda:0"):
+    """Scratch for the device entry points: pd_scratch_bytes(N, x_count, path) — the diagonals
+    of the X-mask range plus their non-finite flags — as a complex128 tensor."""
+    import torch
+    nbytes = pd.device.scratch_bytes(nq, 2**nq if x_count is None else x_count, path)
+    return torch.empty((nbytes + 15) // 16, dtype=torch.complex128, device=device)
+
+
 def same_values(a, b):
     """Equal as complex numbers (IEEE ==, so -0.0 == +0.0; SURVEY §7 signed zeros)."""
     a = np.asarray(a)
     b = np.asarray(b)
     return a.shape == b.shape and bool(np.all(a == b))
+
+
+def same_or_both_nan(a, b):
+    """Equal values with NaN in the same places (part by part; NaN payloads are not compared:
+    x86 and CUDA generate different default NaNs). IEEE == otherwise, so -0.0 == +0.0."""
+    a = np.asarray(a, dtype=complex)
+    b = np.asarray(b, dtype=complex)
+    return a.shape == b.shape and all(
+        np.array_equal(p, q, equal_nan=True) for p, q in ((a.real, b.real), (a.imag, b.imag)))

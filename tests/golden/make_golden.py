@@ -90,6 +90,27 @@ def main() -> None:
     out["batch8_ns"] = ns
     out["batch8_coeffs"] = np.array([ref.coefficient(g, int(n)) for n in ns])
 
+    # non-finite elements: the reference multiplies lambda * a[...] as std::complex<double>
+    # (decompose.cpp:40), so 0 * inf terms are NaN; inf / -inf / NaN sprinkled over seeded N(0,1)
+    # matrices N=1..6, with the reference's decompose (both drivers), coefficient(slow) and
+    # recompose of the result
+    kat_nf = np.array([[1, np.inf], [3, 4]], dtype=complex)
+    out["nfkat_matrix"] = kat_nf
+    out["nfkat_coeffs"] = ref.decompose(kat_nf)
+    specials = np.array([np.inf, -np.inf, np.nan, 0.0, -0.0])
+    rng = np.random.default_rng(4040)
+    for k, nq in enumerate((1, 1, 2, 2, 3, 3, 4, 5, 6)):
+        g = normal_matrix(rng, nq)
+        for _ in range(int(rng.integers(1, 4))):
+            i = int(rng.integers(0, 4**nq))
+            part = g.real if rng.random() < 0.5 else g.imag
+            part.flat[i] = rng.choice(specials)
+        out[f"nf{k}_matrix"] = g
+        out[f"nf{k}_coeffs"] = ref.decompose(g)
+        out[f"nf{k}_serial"] = ref.decompose(g, serial=True)
+        out[f"nf{k}_slow"] = np.array([ref.coefficient(g, n, slow=True) for n in range(min(4**nq, 64))])
+        out[f"nf{k}_recomposed"] = ref.recompose(out[f"nf{k}_coeffs"])
+
     # label helpers (module.cpp:108-114)
     labels = ["I", "X", "Y", "Z", "XY", "IX", "ZZ", "IXZY", "YYYYY", "ZIXYIZ"]
     out["labels"] = np.array(labels)

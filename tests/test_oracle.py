@@ -8,7 +8,7 @@ this container — the reference library compiled from its own sources (oracle/_
 import numpy as np
 import pytest
 
-from conftest import normal_matrix, same_values
+from conftest import normal_matrix, same_or_both_nan, same_values
 from oracle import oracle as O
 
 
@@ -147,3 +147,52 @@ def test_compiled_reference_matches_its_own_golden(ref, golden):
     assert same_values(ref.coeff_batch(golden["batch8_matrix"], golden["batch8_ns"]),
                        golden["batch8_coeffs"])
     assert ref.matrix_seed(20260823, 14, 0) == seed
+
+
+def test_nonfinite_elements_match_reference_golden(port, golden):
+    """Non-finite elements follow the reference's complex product (decompose.cpp:40): 0 * inf
+    is NaN in the other component, and libgcc's Annex G recovery when both parts are NaN.
+    [[1, inf], [3, 4]] -> [2.5, inf + nan i, nan + inf i, -1.5]."""
+    got = port.decompose(golden["nfkat_matrix"], threads=1)
+    assert same_or_both_nan(got, golden["nfkat_coeffs"])
+    assert np.isnan(got[1].imag) and got[1].real == np.inf
+    assert np.isnan(got[2].real) and got[2].imag == np.inf
+    k = 0
+    while f"nf{k}_matrix" in golden:
+        g = golden[f"nf{k}_matrix"]
+        want = golden[f"nf{k}_coeffs"]
+        assert same_or_both_nan(port.decompose(g), want), k
+        assert same_or_both_nan(want, golden[f"nf{k}_serial"]), k
+        slow = golden[f"nf{k}_slow"]
+        assert same_or_both_nan([port.coeff_slow(g, n) for n in range(slow.size)], slow), k
+        assert same_or_both_nan(port.coeff_batch(g, np.arange(want.size, dtype=np.uint64)), want)
+        assert same_or_both_nan(port.recompose(want), golden[f"nf{k}_recomposed"]), k
+        k += 1
+    assert k >= 8
+
+
+def test_nonfinite_elements_match_compiled_reference(port, ref):
+    """Every special value (+-0, +-inf, NaN, in either part) at every position of 2x2 matrices,
+    and random sprinkles up to N=5, against the reference library itself."""
+    specials = [0.0, -0.0, 1.5, -2.0, np.inf, -np.inf, np.nan]
+    rng = np.random.default_rng(41)
+    for pos in range(4):
+        for re in specials:
+            for im in specials:
+                g = normal_matrix(rng, 1)
+                g.real.flat[pos] = re
+                g.imag.flat[pos] = im
+                a = ref.decompose(g, threads=1)
+                assert same_or_both_nan(port.decompose(g, threads=1), a), (pos, re, im)
+                for n in range(4):
+                    assert same_or_both_nan(port.coeff_slow(g, n), ref.coeff_slow(g, n))
+                assert same_or_both_nan(port.recompose(a), ref.recompose(a))
+    for trial in range(200):
+        nq = int(rng.integers(1, 6))
+        g = normal_matrix(rng, nq)
+        for _ in range(int(rng.integers(1, 4))):
+            part = g.real if rng.random() < 0.5 else g.imag
+            part.flat[int(rng.integers(0, 4**nq))] = rng.choice(specials)
+        a = ref.decompose(g)
+        assert same_or_both_nan(port.decompose(g), a), (trial, nq)
+        assert same_or_both_nan(port.recompose(a), ref.recompose(a)), (trial, nq)

@@ -8,7 +8,7 @@ an exact zero may differ). The WHT path is held to the tolerance.
 import numpy as np
 import pytest
 
-from conftest import ROOT, normal_matrix, same_values
+from conftest import ROOT, device_scratch, normal_matrix, same_values
 from oracle import oracle as O
 
 pytestmark = pytest.mark.gpu
@@ -128,7 +128,7 @@ def test_host_pipeline_matches_device_path(pd, cuda, nq, path):
     g = normal_matrix(np.random.default_rng(1300 + nq), nq)
     gd = torch.from_numpy(g).to(cuda)
     out = torch.empty(4**nq, dtype=torch.complex128, device=cuda)
-    scratch = torch.empty(4**nq, dtype=torch.complex128, device=cuda)
+    scratch = device_scratch(pd, nq, path="wht")
     pd.device.decompose(nq, gd.data_ptr(), out.data_ptr(), scratch.data_ptr(), path, 0)
     torch.cuda.synchronize()
     assert np.array_equal(pd.decompose(g, path=path), out.cpu().numpy())
@@ -196,11 +196,11 @@ def test_sharded_runs_assemble_full_array(pd, cuda):
     nq = 9
     g = torch.from_numpy(normal_matrix(np.random.default_rng(8), nq)).to(cuda)
     full = torch.empty(4**nq, dtype=torch.complex128, device=cuda)
-    scratch = torch.empty(4**nq, dtype=torch.complex128, device=cuda)
+    scratch = device_scratch(pd, nq, path="wht")
     pd.device.decompose(nq, g.data_ptr(), full.data_ptr(), scratch.data_ptr(), "gray", 0)
     for p in (1, 2, 3, 5, 8):
         xc = 2 ** (nq - p)
-        diag = torch.empty(max(xc, 32) * 2**nq, dtype=torch.complex128, device=cuda)
+        diag = device_scratch(pd, nq, max(xc, 32))
         packed = torch.empty(4**nq >> p, dtype=torch.complex128, device=cuda)
         out = torch.zeros_like(full)
         out_runs = torch.zeros_like(full)
@@ -238,7 +238,7 @@ def test_xmask_range_validation(pd, cuda):
     nq = 6
     g = torch.zeros((64, 64), dtype=torch.complex128, device=cuda)
     out = torch.empty(4**nq, dtype=torch.complex128, device=cuda)
-    diag = torch.empty(64 * 64, dtype=torch.complex128, device=cuda)
+    diag = device_scratch(pd, nq, 64)
     with pytest.raises(ValueError):   # spans two blocks of 2^(N-p)
         pd.device.shard_coeffs(nq, g.data_ptr(), 0, 64, 1, out.data_ptr(), "runs", diag.data_ptr())
     with pytest.raises(ValueError):   # run_bits > 8
@@ -265,7 +265,7 @@ def test_n14_config5(pd, cuda, port, golden):
     assert torch.equal(flat[-4096:].cpu(), torch.from_numpy(golden["unif14_tail"]))
     assert torch.equal(flat[idx].cpu(), torch.from_numpy(golden["unif14_at_idx"]))
     out = torch.empty(4**nq, dtype=torch.complex128, device=cuda)
-    scratch = torch.empty(4**nq, dtype=torch.complex128, device=cuda)
+    scratch = device_scratch(pd, nq, path="wht")
     pd.device.decompose(nq, g.data_ptr(), out.data_ptr(), scratch.data_ptr(), "gray", 0)
     torch.cuda.synchronize()
     ns = golden["unif14_ns"].astype(np.int64)
@@ -312,7 +312,7 @@ def test_n15_maximum_single_gpu_size(pd, cuda):
     g = torch.empty((2**nq, 2**nq), dtype=torch.complex128, device=cuda)
     pd.device.random_matrix(nq, 1515, g.data_ptr(), 0)
     out = torch.empty(4**nq, dtype=torch.complex128, device=cuda)
-    scratch = torch.empty(4**nq, dtype=torch.complex128, device=cuda)
+    scratch = device_scratch(pd, nq, path="wht")
     pd.device.decompose(nq, g.data_ptr(), out.data_ptr(), scratch.data_ptr(), "gray", 0)
     ns = torch.from_numpy(np.sort(np.random.default_rng(15).choice(4**nq, 65536, replace=False))
                           .astype(np.int64)).to(cuda)
@@ -378,7 +378,7 @@ def test_blocked_scratch_matches_one_shot(pd, cuda):
     nq = 11
     g = torch.from_numpy(normal_matrix(np.random.default_rng(11), nq)).to(cuda)
     full = torch.empty(4**nq, dtype=torch.complex128, device=cuda)
-    scratch = torch.empty(4**nq, dtype=torch.complex128, device=cuda)
+    scratch = device_scratch(pd, nq, path="wht")
     for path in ("gray", "wht"):
         pd.device.decompose(nq, g.data_ptr(), full.data_ptr(), scratch.data_ptr(), path, 0)
         for blocks in (2, 8, 64):
@@ -406,7 +406,7 @@ def test_n16_on_one_gpu_with_blocked_scratch(pd, cuda):
     g = torch.empty((2**nq, 2**nq), dtype=torch.complex128, device=cuda)
     pd.device.random_matrix(nq, 1616, g.data_ptr(), 0)
     out = torch.empty(4**nq, dtype=torch.complex128, device=cuda)
-    scratch = torch.empty(4096 * 2**nq, dtype=torch.complex128, device=cuda)
+    scratch = device_scratch(pd, nq, 4096)
     pd.device.decompose_blocked(nq, g.data_ptr(), out.data_ptr(), scratch.data_ptr(),
                                 scratch.numel() * 16, "gray", 0)
     ns = torch.from_numpy(np.sort(np.random.default_rng(16).choice(4**nq, 2048, replace=False))
@@ -604,3 +604,98 @@ print("ok")
 ''' % ROOT
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
+
+
+def test_k2s_c_shards_run_bits_n14(pd, cuda):
+    """The kernel configuration every rank of a 2/4/8-GPU run executes at N=14: K2s-c (each
+    rank's 8192 / 4096 / 2048 X-masks exceed gray_share_c_min_xmasks(14)) with run_bits 1..3,
+    in both output layouts (rank 0 writes GLOBAL in place, the others pack RUNS). Emulated shard
+    by shard on one GPU and compared bit for bit with the one-shot decomposition."""
+    import torch
+    nq = 14
+    g = torch.empty((2**nq, 2**nq), dtype=torch.complex128, device=cuda)
+    pd.device.random_matrix(nq, pd.matrix_seed(20260823, nq, 0), g.data_ptr(), 0)
+    full = torch.empty(4**nq, dtype=torch.complex128, device=cuda)
+    scratch = device_scratch(pd, nq)
+    pd.device.decompose(nq, g.data_ptr(), full.data_ptr(), scratch.data_ptr(), "gray", 0)
+    out = torch.empty_like(full)
+    for p in (1, 2, 3):
+        xc = 2 ** (nq - p)
+        rl = 4 ** (nq - p)
+        packed = torch.empty(4**nq >> p, dtype=torch.complex128, device=cuda)
+        out.zero_()
+        for shard in range(2**p):
+            pd.device.diag_gather(nq, g.data_ptr(), shard * xc, xc, scratch.data_ptr(), 0)
+            if shard == 0:   # rank 0: GLOBAL, in place
+                pd.device.xmask_coeffs(nq, scratch.data_ptr(), 0, xc, p, out.data_ptr(), "global",
+                                       "gray", 0)
+            else:            # the other ranks: RUNS, packed for the gather
+                pd.device.xmask_coeffs(nq, scratch.data_ptr(), shard * xc, xc, p, packed.data_ptr(),
+                                       "runs", "gray", 0)
+                for r in range(2**p):
+                    o = pd.device.run_offset(nq, p, shard, r)
+                    out[o:o + rl] = packed[r * rl:(r + 1) * rl]
+        torch.cuda.synchronize()
+        assert torch.equal(out, full), p
+        # and every shard in the other layout too
+        out.zero_()
+        for shard in range(2**p):
+            pd.device.diag_gather(nq, g.data_ptr(), shard * xc, xc, scratch.data_ptr(), 0)
+            if shard == 0:
+                pd.device.xmask_coeffs(nq, scratch.data_ptr(), 0, xc, p, packed.data_ptr(), "runs",
+                                       "gray", 0)
+                for r in range(2**p):
+                    o = pd.device.run_offset(nq, p, 0, r)
+                    out[o:o + rl] = packed[r * rl:(r + 1) * rl]
+            else:
+                pd.device.xmask_coeffs(nq, scratch.data_ptr(), shard * xc, xc, p, out.data_ptr(),
+                                       "global", "gray", 0)
+        torch.cuda.synchronize()
+        assert torch.equal(out, full), p
+        del packed
+
+
+def test_k2s_c_segment_host_pipeline_n15(pd, cuda):
+    """N=15 through the host API: the pipeline's final-segment launches (1024 X-masks per
+    download block >= gray_share_c_min_xmasks(15)) run the K2s-c segment instantiation
+    (pd_k2cseg.cu); the result must equal the device-resident one-shot decomposition."""
+    import torch
+    nq = 15
+    torch.cuda.empty_cache()
+    if torch.cuda.mem_get_info()[0] < 120 * 2**30:
+        pytest.skip("needs ~112 GiB of free device memory")
+    g = torch.empty((2**nq, 2**nq), dtype=torch.complex128, device=cuda)
+    pd.device.random_matrix(nq, 1515, g.data_ptr(), 0)
+    out = torch.empty(4**nq, dtype=torch.complex128, device=cuda)
+    scratch = device_scratch(pd, nq)
+    pd.device.decompose(nq, g.data_ptr(), out.data_ptr(), scratch.data_ptr(), "gray", 0)
+    torch.cuda.synchronize()
+    del scratch
+    gh = g.cpu().numpy()
+    del g
+    torch.cuda.empty_cache()
+    host = pd.decompose(gh)
+    del gh
+    want = out.cpu().numpy()
+    assert np.array_equal(host.view(np.uint64), want.view(np.uint64))
+
+
+def test_full_n12_config4_full_array(pd, cuda, port):
+    """BASELINE configs[3]: every one of the 16,777,216 coefficients of an N=12 N(0,1) matrix
+    equal to the oracle (IEEE ==), through the host API and the serial driver alias"""
+    g = normal_matrix(np.random.default_rng(412), 12)
+    want = port.decompose(g)
+    assert same_values(pd.decompose(g), want)
+    assert same_values(pd.decompose(g, serial=True, threads=0), want)
+
+
+@pytest.mark.parametrize("nq", range(1, 7))
+def test_serial_quaternary_driver(pd, cuda, golden, nq):
+    """decompose(g, serial=True) (module.cpp:56-60 -> decompose_serial_quaternary,
+    decompose.cpp:133-152) gives the reference's serial output; it ignores `threads`, and the
+    parallel driver rejects threads=0 (decompose.cpp:98-99)"""
+    g = golden[f"normal{nq}_matrix"]
+    assert same_values(pd.decompose(g, serial=True), golden[f"normal{nq}_serial"])
+    assert same_values(pd.decompose(g, threads=0, serial=True), golden[f"normal{nq}_serial"])
+    with pytest.raises(ValueError):
+        pd.decompose(g, threads=0)

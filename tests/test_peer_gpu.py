@@ -46,7 +46,8 @@ def _worker(rank, world, port, nq, path, result_path):
     ok = True
     if rank == 0:
         want = torch.empty_like(out)
-        scratch = torch.empty(4**nq, dtype=torch.complex128, device=dev)
+        nb = pd.device.scratch_bytes(nq, 2**nq, path)
+        scratch = torch.empty((nb + 15) // 16, dtype=torch.complex128, device=dev)
         pd.device.decompose(nq, G.data_ptr(), want.data_ptr(), scratch.data_ptr(), path,
                             torch.cuda.current_stream().cuda_stream)
         torch.cuda.synchronize()
