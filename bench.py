@@ -41,9 +41,11 @@ def parse_args():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--qubits", type=int, default=14)
     ap.add_argument("--path", choices=["gray", "wht"], default="gray")
-    ap.add_argument("--mode", choices=["nccl", "peer"], default="nccl",
-                    help="N>1 data path: NCCL broadcast + gather (north star) or CUDA-IPC peer "
-                         "memory (K1 reads rank 0's G, K2 stores into rank 0's output)")
+    ap.add_argument("--mode", choices=["nccl", "nccl-serial", "peer"], default="nccl",
+                    help="N>1 data path: NCCL pipeline (diagonal chunks scattered in walk order, "
+                         "sub-blocks gathered while the next computes), serial NCCL broadcast + "
+                         "gather, or CUDA-IPC peer memory (K1 reads rank 0's G, K2 stores into "
+                         "rank 0's output)")
     ap.add_argument("--sample-masks", type=int, default=64,
                     help="X-masks in the CPU sample (>= 8); 64 = 1,048,576 coefficients, ~10 s on 16 threads")
     ap.add_argument("--no-e2e", action="store_true")
@@ -61,10 +63,13 @@ def workload_config(nq: int, world: int, path: str, mode: str = "nccl") -> dict:
         "matrix": f"random_matrix({nq}, matrix_seed({ACCEPT_SEED},{nq},0)): uniform[-1,1) complex128, "
                   f"{16 * 4**nq / 2**30:g} GiB (reference generator, bit-exact on device)",
         "path": "gray-code K1+K2" if path == "gray" else "walsh-hadamard K1+K4",
-        "parallelism": f"xmask-shard x{world}" + ((" (NCCL broadcast G + grouped send/recv gather)"
-                                                    if mode == "nccl" else
-                                                    " (CUDA-IPC peer memory: K1 reads rank 0's G, K2 stores into rank 0's output)")
-                                                   if world > 1 else ""),
+        "parallelism": f"xmask-shard x{world}" + ({
+            "nccl": " (NCCL pipeline: rank 0 gathers each rank's diagonals one walk chunk at a time and "
+                    "sends them in walk order, walk segments chase the chunks, finished sub-blocks "
+                    "are sent to rank 0 while the next computes)",
+            "nccl-serial": " (NCCL broadcast G + grouped send/recv gather)",
+            "peer": " (CUDA-IPC peer memory: K1 reads rank 0's G, K2 stores into rank 0's output)",
+        }[mode] if world > 1 else ""),
         "l2": "inputs (4 GiB G, 4 GiB diagonals) exceed the 126 MB L2; no flush needed" if nq >= 12
         else "inputs smaller than L2",
     }
@@ -244,57 +249,47 @@ def run_ours(args) -> None:
     pd_seed = pd.matrix_seed(ACCEPT_SEED, nq, 0)  # the reference generator's seed (bench.cpp:42-46)
     if rank == 0:
         pd.device.random_matrix(nq, pd_seed, G.data_ptr(), sptr)
-    from paper_2401_16378_b200.sharding import scratch_tensor
-    diag = scratch_tensor(nq, plan.x_count, args.path, dev)  # diagonals + non-finite flags
+    from paper_2401_16378_b200.sharding import ShardedDecomposer, scratch_tensor
     out = torch.empty(4**nq, dtype=torch.complex128, device=dev) if rank == 0 else None
-    peer = args.mode == "peer" and world > 1
-    local = None if rank == 0 or peer else torch.empty(plan.run_len << plan.run_bits,
-                                                       dtype=torch.complex128, device=dev)
-    from paper_2401_16378_b200.sharding import ShardedDecomposer
-    # the sharding layer's collectives (NCCL gather / peer mapping); K1 and K2 are launched here
-    # so that they can be timed apart
-    sd = ShardedDecomposer(nq, dev, mode=args.mode, path=args.path, buffers=False)
-    if peer:
-        # rank 0's G and output mapped into every rank once (CUDA IPC), outside the timed region
-        g_src, dst = sd.peer_buffers(G, out)
-        layout = "global"
-        torch.cuda.synchronize()
-        barrier()
+    if world == 1:
+        # one GPU: K1 and K2 launched here so that they can be timed apart
+        diag = scratch_tensor(nq, plan.x_count, args.path, dev)
+        sd = None
     else:
-        # rank 0 writes its runs in place in the reference-ordered array; the others pack theirs
-        g_src = G
-        dst, layout = (out, "global") if rank == 0 else (local, "runs")
-        sd.local = local
-
-    def gather():
-        if world == 1:
-            return
-        if peer:  # the peers' K2 stores landed in rank 0's output; order them before its reads
+        # the sharding layer: NCCL pipeline (diagonal chunks scattered in walk order, walk
+        # segments chasing them, finished sub-blocks gathered while the next computes), the
+        # serial NCCL mode, or CUDA-IPC peer memory
+        diag = None
+        sd = ShardedDecomposer(nq, dev, mode=args.mode, path=args.path)
+        if sd.mode == "peer":   # rank 0's G and output mapped once, outside the timed region
+            sd.peer_buffers(G, out)
             torch.cuda.synchronize()
             barrier()
-            return
-        sd.gather(out)
 
     def step(path, ev=None):
-        if world > 1 and not peer:
-            dist.broadcast(G, src=0)
         if ev is not None:
             ev[0].record(stream)
-        gp, dp = sd_ptr(g_src), sd_ptr(dst)
+        if world > 1:  # the whole sharded step (its kernels and transfers on the layer's streams)
+            if ev is not None:
+                ev[1].record(stream)
+            sd(G, out)
+            if ev is not None:
+                ev[2].record(stream)
+            return
+        gp, dp = G.data_ptr(), out.data_ptr()
         if path == "gray":  # K1 and K2 timed separately
             pd.device.diag_gather(nq, gp, plan.x0, plan.x_count, diag.data_ptr(), sptr)
             if ev is not None:
                 ev[1].record(stream)
             pd.device.xmask_coeffs(nq, diag.data_ptr(), plan.x0, plan.x_count, plan.run_bits,
-                                   dp, layout, path, sptr)
+                                   dp, "global", path, sptr)
         else:  # fused two-pass WHT straight from G
             if ev is not None:
                 ev[1].record(stream)
             pd.device.shard_coeffs(nq, gp, plan.x0, plan.x_count, plan.run_bits,
-                                   dp, layout, diag.data_ptr(), path, sptr)
+                                   dp, "global", diag.data_ptr(), path, sptr)
         if ev is not None:
             ev[2].record(stream)
-        gather()
 
     def timed(path, steps, warmup, sample_clocks=False):
         for _ in range(warmup):
@@ -356,7 +351,17 @@ def run_ours(args) -> None:
                                    f"{sm_max:g} MHz (MEASURED_PEAKS.json has no FP64 entry)",
                     "probe_tflops": probe / 1e12, "frac_of_probe": achieved / (probe / 1e12),
                     "k1_gather_ms": k1_ms, "k2_ms": k2_ms,
-                    "k1_gather_gbs": 32.0 * 4**nq / world / (k1_ms / 1e3) / 1e9}
+                    "k1_gather_gbs": 32.0 * 4**nq / world / (k1_ms / 1e3) / 1e9 if k1_ms > 0 else None}
+        if world > 1:
+            roofline["timed"] = ("the whole sharded step on each rank (its K1/K2 segments and the NCCL "
+                                 "transfers they overlap), max over ranks: a lower bound on the kernel's rate")
+            roofline["k2_ms"] = k2_ms = ms / args.steps
+            roofline.pop("k1_gather_ms")
+            roofline.pop("k1_gather_gbs")
+            roofline["achieved"] = achieved = dadd / (k2_ms / 1e3) / 1e12
+            roofline["frac"] = achieved / peak
+            roofline["frac_of_probe"] = achieved / (probe / 1e12)
+            roofline["reference_walk_equiv_tflops"] = ref_dadd / (k2_ms / 1e3) / 1e12
     else:
         byts = 32.0 * 4**nq / world
         achieved = byts / ((k1_ms + k2_ms) / 1e3) / 1e9
@@ -370,7 +375,7 @@ def run_ours(args) -> None:
         "ms_per_step": per_step_ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": workload_config(nq, world, args.path, args.mode),
+        "config": workload_config(nq, world, args.path, sd.mode if sd is not None else args.mode),
         "roofline": roofline,
         "gpu_launches": launches,
         "clocks": clocks,
@@ -409,8 +414,8 @@ def run_ours(args) -> None:
 
     # ---- e2e through the public API with pinned host buffers (H2D + D2H inside)
     if not args.no_e2e:
-        del diag, local
-        e2e = run_e2e(args, pd, plan, G, out, dev, stream, barrier, max_over_ranks, world, rank)
+        del diag
+        e2e = run_e2e(args, pd, plan, G, out, dev, stream, barrier, max_over_ranks, world, rank, sd)
         wht_e2e = e2e.pop("wht_path_e2e", None)
         line["e2e"] = e2e
         if wht_e2e is not None and "wht_path" in line:
@@ -493,7 +498,7 @@ def side_configs(pd, dev, stream, sptr, peaks):
     return res
 
 
-def run_e2e(args, pd, plan, G, out, dev, stream, barrier, max_over_ranks, world, rank):
+def run_e2e(args, pd, plan, G, out, dev, stream, barrier, max_over_ranks, world, rank, sd=None):
     """The user-facing call on host memory. N=1: paper_2401_16378_b200.decompose(G_host, out=...)
     (C ABI pd_decompose: H2D, K1, K2, D2H). N>1: rank 0 uploads G, ShardedDecomposer runs the
     broadcast/compute/gather, rank 0 downloads the coefficients."""
@@ -531,7 +536,8 @@ def run_e2e(args, pd, plan, G, out, dev, stream, barrier, max_over_ranks, world,
                                    "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes}
         return res
     from paper_2401_16378_b200.sharding import ShardedDecomposer
-    sd = ShardedDecomposer(nq, dev, path=args.path, mode=args.mode)
+    if sd is None:
+        sd = ShardedDecomposer(nq, dev, path=args.path, mode=args.mode)
     gh_t = oh_t = None
     if rank == 0:
         gh_t = torch.empty(G.shape, dtype=torch.complex128, pin_memory=True)
@@ -562,12 +568,36 @@ def run_e2e(args, pd, plan, G, out, dev, stream, barrier, max_over_ranks, world,
             "api": "paper_2401_16378_b200.sharding.ShardedDecomposer with pinned host G/out on rank 0"}
 
 
+def free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def self_launch(args) -> int:
+    """`bench.py --gpus N` without a torchrun environment: start the N ranks (one process per
+    GPU) under torch.distributed.run on this node, 127.0.0.1 rendezvous, same arguments."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse_args()
     if args.impl == "reference":
         run_reference_arm(args)
-    else:
-        run_ours(args)
+        return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(self_launch(args))
+    if args.gpus > 1:
+        # NCCL's communicator setup on stderr (stdout keeps rank 0's one JSON line): rank and
+        # nranks of every communicator, for the driver's check
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    run_ours(args)
 
 
 if __name__ == "__main__":

@@ -129,3 +129,131 @@ def test_plan_rejects_bad_world_sizes():
     p = ShardPlan(6, 8, 5)
     assert (p.run_bits, p.x_count, p.x0, p.run_len) == (3, 8, 40, 64)
     assert sorted(o for g in range(8) for o in p.offsets(g)) == list(range(0, 4**6, 64))
+
+
+# ---------------------------------------------------------------------------------------------
+# the pipelined NCCL mode's schedule (sharding.NcclPipeline) with numpy stand-ins of its device
+# primitives: which diagonal pieces go to which rank in which order, the segment chaining and the
+# sub-block packing / unpacking of the runs. The stand-in walk sums in a different order (a
+# matrix product), so results are compared to the oracle within 1e-12.
+
+class CpuPipelineOps:
+    """numpy restatements of the pipeline's device primitives (include/pd_api.h)"""
+
+    def begin(self):
+        pass
+
+    def end(self):
+        pass
+
+    def on(self, name):
+        import contextlib
+        return contextlib.nullcontext()
+
+    def record(self, name):
+        return None
+
+    def wait(self, name, ev):
+        pass
+
+    def segment_chunks(self, N, chunk_log):
+        return (1 << N) >> chunk_log if chunk_log < N else 0
+
+    def gather_tiled(self, st, N, G, x0, x_count, col0, cols, xb_log, cb_log, out):
+        dim = 1 << N
+        g = G.reshape(dim, dim).numpy()
+        o = out.numpy()
+        xl = np.arange(x_count, dtype=np.int64)[:, None]
+        i = np.arange(col0, col0 + cols, dtype=np.int64)[None, :]
+        blk = ((xl >> xb_log) << (N - cb_log)) + (i >> cb_log)
+        at = (((blk << xb_log) | (xl & ((1 << xb_log) - 1))) << cb_log) | (i & ((1 << cb_log) - 1))
+        o[at] = g[i ^ (x0 + xl), i]
+
+    def place_cols(self, st, N, packed, x_count, col0, cols, diag):
+        dim = 1 << N
+        d = diag.numpy()[:x_count * dim].reshape(x_count, dim)
+        d[:, col0:col0 + cols] = packed.numpy()[:x_count * cols].reshape(x_count, cols)
+
+    def segment(self, st, N, diag, x0, x_count, chunk_log, c0, c1, part_in, part_out, run_bits, out,
+                layout):
+        from oracle import oracle as O
+        dim = 1 << N
+        C = 1 << chunk_log
+        c1 = c1 or dim // C
+        ks = np.arange(c0 * C, c1 * C, dtype=np.int64)
+        gk = ks ^ (ks >> 1)
+        z = np.arange(dim, dtype=np.int64)
+        sign = 1.0 - 2.0 * (np.bitwise_count(gk[:, None] & z[None, :]) & 1)
+        D = diag.numpy()[:x_count * dim].reshape(x_count, dim)
+        S = D[:, gk] @ sign
+        if part_in is not None:
+            S = S + part_in.numpy()[:x_count * dim].reshape(x_count, dim)
+        if part_out is not None:
+            part_out.numpy()[:x_count * dim] = S.reshape(-1)
+            return
+        o = out.numpy()
+        low = 2 * (N - run_bits)
+        for xl in range(x_count):
+            x = x0 + xl
+            ns = O.xz_to_n(np.uint64(x), z.astype(np.uint64), N).astype(np.int64)
+            c = (-1j) ** np.bitwise_count(x & z) * S[xl] / dim
+            if layout == "global":
+                o[ns] = c
+            else:
+                o[((z >> (N - run_bits)) << low) | (ns & ((1 << low) - 1))] = c
+
+    def copy_runs(self, st, src, dst, run_len, src_off, dst_off):
+        for a, b in zip(src_off.tolist(), dst_off.tolist()):
+            dst[b:b + run_len] = src[a:a + run_len]
+
+    def offsets(self, values):
+        return torch.tensor(values, dtype=torch.int64)
+
+
+def _pipeline_worker(rank, world, port, nq, chunk_log, sub_bits, result_path):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2401_16378_b200.sharding import ShardedDecomposer
+    from oracle import oracle as O
+    dim = 2**nq
+    if rank == 0:
+        G = torch.from_numpy(O.port().random_matrix(nq, 4343))
+        out = torch.full((4**nq,), complex(np.nan, np.nan), dtype=torch.complex128)
+    else:
+        G = torch.full((dim, dim), complex(np.nan, np.nan), dtype=torch.complex128)  # never read
+        out = None
+    sd = ShardedDecomposer(nq, torch.device("cpu"), mode="nccl", pipeline_ops=CpuPipelineOps(),
+                           pipeline_chunk_log=chunk_log, pipeline_sub_bits=sub_bits)
+    assert sd.mode == "nccl" and sd.pipeline is not None
+    for _ in range(2):
+        sd(G, out)
+    if rank == 0:
+        np.save(result_path, out.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,nq,chunk_log,sub_bits", [(2, 6, 2, 2), (4, 6, 2, 1), (8, 7, 3, 1),
+                                                         (4, 8, 4, 2)])
+def test_nccl_pipeline_schedule_matches_oracle(tmp_path, world, nq, chunk_log, sub_bits):
+    result = str(tmp_path / "out.npy")
+    mp.start_processes(_pipeline_worker, args=(world, _free_port(), nq, chunk_log, sub_bits, result),
+                       nprocs=world, join=True, start_method="spawn")
+    got = np.load(result)
+    import sys
+    sys.path.insert(0, ROOT)
+    from oracle import oracle as O
+    want = O.port().decompose(O.port().random_matrix(nq, 4343))
+    assert np.all(np.isfinite(got))
+    assert np.max(np.abs(got - want)) <= 1e-12 * np.max(np.abs(want))
+
+
+def test_walk_segments_cover_the_walk():
+    from paper_2401_16378_b200.sharding import walk_segments
+    for nch in (4, 8, 16, 32, 64):
+        b = walk_segments(nch)
+        assert b[0] == 0 and b[-1] == nch and b[-2] == nch // 2
+        assert all(x < y for x, y in zip(b, b[1:]))
+        assert b[1:5] == [1, 2, 3, 4][:len(b[1:5])] or nch < 8
