@@ -25,7 +25,7 @@ def test_library_exports_every_declared_symbol(pd):
     missing = [s for s in syms if not hasattr(lib, s)]
     assert not missing, missing
     lib.pd_api_version.restype = ctypes.c_int
-    assert lib.pd_api_version() == 2
+    assert lib.pd_api_version() == 3
     lib.pd_last_error.restype = ctypes.c_char_p
 
 
