@@ -195,42 +195,11 @@ PD_EXPORT int pd_host_alloc(size_t bytes, void** out);
 PD_EXPORT int pd_host_free(void* p);
 
 /* ---------------- NCCL pipeline pieces (multi-GPU sharding, sharding.py) ----------------
- * The pipelined NCCL mode splits the X-masks over P = 2^p ranks like pd_xmask_coeffs_device's
- * run addressing, but moves only what each rank reads: rank 0 gathers the diagonals of every
- * rank (K1, tiled layout) one walk chunk of columns at a time and sends each rank its piece as
- * one message; a rank walks each chunk as it arrives (segments chained through raw partial
- * sums, bit-identical to one launch) and sends each finished sub-block of X-masks back while
- * the next computes. The reference's own parallel split is decompose.cpp:95-131. */
-
-/* K1 for X-masks [x0, x0 + x_count) and columns [col0, col0 + cols) into the tiled layout:
- * blocks of 2^xb_log X-masks x 2^cb_log columns, each block contiguous and X-mask-major inside,
- * blocks ordered X-mask block first: element (x, i), xl = x - x0, lands at
- *   ((((xl >> xb_log) * 2^(N-cb_log) + (i >> cb_log)) * 2^xb_log + xl % 2^xb_log) * 2^cb_log
- *    + i % 2^cb_log)
- * (complex elements; out spans x_count * 2^N). xb_log = log2(x_count), cb_log = N is the
- * row-major layout of pd_diag_gather_device. Ranges are aligned powers of two. */
-PD_EXPORT int pd_diag_gather_tiled_device(unsigned num_qubits, const double* g, uint64_t x0,
-                                          uint64_t x_count, uint64_t col0, uint64_t cols,
-                                          unsigned xb_log, unsigned cb_log, double* out, void* stream);
-
-/* Copy a packed column block — x_count rows of `cols` elements, row after row (one block of the
- * tiled layout) — into columns [col0, col0 + cols) of row-major diagonals diag[x_count][2^N]. */
-PD_EXPORT int pd_place_cols_device(unsigned num_qubits, const double* packed, uint64_t x_count,
-                                   uint64_t col0, uint64_t cols, double* diag, void* stream);
-
-/* Walk chunks the segment form uses for chunk_log (0 when N is too small to segment). */
-PD_EXPORT unsigned pd_gray_segment_chunks(unsigned num_qubits, unsigned chunk_log);
-
-/* The Gray walk over chunks [c_begin, c_end) of 2^chunk_log steps (c_end = 0: to the end) for
- * the X-masks [x0, x0 + x_count) of diag (row-major, row 0 = X-mask x0): continues from the raw
- * sums part_in (NULL: from zero) and stores raw sums to part_out (x_count * 2^N complex), or —
- * part_out == NULL — the finished coefficients with the output addressing of
- * pd_xmask_coeffs_device. Chaining segments keeps every coefficient's summation order, so the
- * result equals one pd_xmask_coeffs_device call bit for bit (same as decompose_parallel). */
-PD_EXPORT int pd_gray_segment_device(unsigned num_qubits, const double* diag, uint64_t x0,
-                                     uint64_t x_count, unsigned chunk_log, unsigned c_begin,
-                                     unsigned c_end, const double* part_in, double* part_out,
-                                     unsigned run_bits, double* out, pd_layout layout, void* stream);
+ * The pipelined NCCL mode splits each rank's X-masks into blocks: rank 0 gathers block j's
+ * diagonals of every rank (pd_diag_gather_device, row-major: one contiguous message per rank),
+ * every rank walks block j as soon as its rows are in (pd_xmask_coeffs_device), and each
+ * finished block's 2^(p+q) coefficient runs go back to rank 0 as one message while the next
+ * block computes. The reference's own parallel split is decompose.cpp:95-131. */
 
 /* dst[dst_off[k] + j] = src[src_off[k] + j] for j < run_len, k < count: packing / unpacking
  * coefficient runs (offset tables are device arrays of element offsets, count <= 65535). */

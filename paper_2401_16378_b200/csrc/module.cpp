@@ -291,34 +291,6 @@ PYBIND11_MODULE(_paulidecomp, m) {
           py::arg("out"), py::arg("layout") = "global", py::arg("scratch") = 0,
           py::arg("path") = "gray", py::arg("stream") = 0,
           "All coefficients of an X-mask range straight from G (one shard's work).");
-    d.def("diag_gather_tiled", [](unsigned N, std::uintptr_t g, std::uint64_t x0, std::uint64_t x_count,
-                                  std::uint64_t col0, std::uint64_t cols, unsigned xb_log,
-                                  unsigned cb_log, std::uintptr_t out, std::uintptr_t stream) {
-        check(pd_diag_gather_tiled_device(N, P<const double>(g), x0, x_count, col0, cols, xb_log,
-                                          cb_log, P<double>(out), P<void>(stream)));
-    }, py::arg("num_qubits"), py::arg("g"), py::arg("x0"), py::arg("x_count"), py::arg("col0"),
-          py::arg("cols"), py::arg("xb_log"), py::arg("cb_log"), py::arg("out"), py::arg("stream") = 0,
-          "K1 into the tiled layout of the NCCL pipeline (pd_diag_gather_tiled_device).");
-    d.def("place_cols", [](unsigned N, std::uintptr_t packed, std::uint64_t x_count,
-                           std::uint64_t col0, std::uint64_t cols, std::uintptr_t diag,
-                           std::uintptr_t stream) {
-        check(pd_place_cols_device(N, P<const double>(packed), x_count, col0, cols, P<double>(diag),
-                                   P<void>(stream)));
-    }, py::arg("num_qubits"), py::arg("packed"), py::arg("x_count"), py::arg("col0"), py::arg("cols"),
-          py::arg("diag"), py::arg("stream") = 0);
-    d.def("gray_segment_chunks", &pd_gray_segment_chunks, py::arg("num_qubits"), py::arg("chunk_log"));
-    d.def("gray_segment", [layout_of](unsigned N, std::uintptr_t diag, std::uint64_t x0,
-                                      std::uint64_t x_count, unsigned chunk_log, unsigned c_begin,
-                                      unsigned c_end, std::uintptr_t part_in, std::uintptr_t part_out,
-                                      unsigned run_bits, std::uintptr_t out, const std::string& layout,
-                                      std::uintptr_t stream) {
-        check(pd_gray_segment_device(N, P<const double>(diag), x0, x_count, chunk_log, c_begin, c_end,
-                                     P<const double>(part_in), P<double>(part_out), run_bits,
-                                     P<double>(out), layout_of(layout), P<void>(stream)));
-    }, py::arg("num_qubits"), py::arg("diag"), py::arg("x0"), py::arg("x_count"), py::arg("chunk_log"),
-          py::arg("c_begin"), py::arg("c_end"), py::arg("part_in"), py::arg("part_out"),
-          py::arg("run_bits"), py::arg("out"), py::arg("layout") = "global", py::arg("stream") = 0,
-          "Gray walk over a range of walk chunks, chained through raw partial sums.");
     d.def("copy_runs", [](std::uintptr_t src, std::uintptr_t dst, std::uint64_t run_len,
                           std::uintptr_t src_off, std::uintptr_t dst_off, std::uint64_t count,
                           std::uintptr_t stream) {

@@ -282,48 +282,6 @@ int pd_diag_gather_device(unsigned N, const double* g, uint64_t x0, uint64_t x_c
     return PD_OK;
 }
 
-int pd_diag_gather_tiled_device(unsigned N, const double* g, uint64_t x0, uint64_t x_count,
-                                uint64_t col0, uint64_t cols, unsigned xb_log, unsigned cb_log,
-                                double* out, void* stream) {
-    if (int rc = check_qubits(N)) return rc;
-    if (!g || !out) return fail(PD_EINVAL, "null buffer");
-    if (int rc = check_device()) return rc;
-    const uint64_t dim = 1ull << N;
-    if (x_count == 0 || (x_count & (x_count - 1)) || x0 % x_count || x0 + x_count > dim)
-        return fail(PD_EINVAL, "X-mask range must be an aligned power-of-two block inside [0, 2^N)");
-    if (cols == 0 || (cols & (cols - 1)) || col0 % cols || col0 + cols > dim)
-        return fail(PD_EINVAL, "column range must be an aligned power-of-two block inside [0, 2^N)");
-    if (cb_log > N || (1ull << xb_log) > x_count || xb_log > 31)
-        return fail(PD_EINVAL, "tile blocks must satisfy 2^xb_log <= x_count and cb_log <= N");
-    cudaError_t e = pdb::launch_diag_gather_tiled(reinterpret_cast<const double2*>(g), N, x0, x_count,
-                                                  col0, cols, xb_log, cb_log,
-                                                  reinterpret_cast<double2*>(out),
-                                                  static_cast<cudaStream_t>(stream));
-    if (e != cudaSuccess) return cuda_fail(e, "diag_gather launch");
-    return PD_OK;
-}
-
-int pd_place_cols_device(unsigned N, const double* packed, uint64_t x_count, uint64_t col0,
-                         uint64_t cols, double* diag, void* stream) {
-    if (int rc = check_qubits(N)) return rc;
-    if (!packed || !diag) return fail(PD_EINVAL, "null buffer");
-    if (int rc = check_device()) return rc;
-    const uint64_t dim = 1ull << N;
-    if (cols == 0 || col0 + cols > dim) return fail(PD_EINVAL, "column range outside [0, 2^N)");
-    if (x_count == 0) return PD_OK;
-    PD_CUDA(cudaMemcpy2DAsync(diag + 2 * col0, dim * sizeof(double2), packed, cols * sizeof(double2),
-                              cols * sizeof(double2), x_count, cudaMemcpyDeviceToDevice,
-                              static_cast<cudaStream_t>(stream)));
-    return PD_OK;
-}
-
-unsigned pd_gray_segment_chunks(unsigned N, unsigned chunk_log) {
-    if (N == 0 || N >= 32 || pdb::gray_xmask_chunks(N) <= 1 || chunk_log >= N || chunk_log < 5 ||
-        chunk_log > 11)
-        return 0;
-    return 1u << (N - chunk_log);
-}
-
 int pd_copy_runs_device(const double* src, double* dst, uint64_t run_len, const uint64_t* src_off,
                         const uint64_t* dst_off, uint64_t count, void* stream) {
     if (int rc = check_device()) return rc;
@@ -377,37 +335,6 @@ int pd_xmask_coeffs_device(unsigned N, const double* diag, uint64_t x0, uint64_t
         default: return fail(PD_EINVAL, "path must be PD_PATH_GRAY or PD_PATH_WHT");
     }
     if (e != cudaSuccess) return cuda_fail(e, "xmask coefficient launch");
-    return PD_OK;
-}
-
-int pd_gray_segment_device(unsigned N, const double* diag, uint64_t x0, uint64_t x_count,
-                           unsigned chunk_log, unsigned c_begin, unsigned c_end,
-                           const double* part_in, double* part_out, unsigned run_bits, double* out,
-                           pd_layout layout, void* stream) {
-    if (int rc = check_qubits(N)) return rc;
-    if (int rc = check_device()) return rc;
-    if (!diag) return fail(PD_EINVAL, "null buffer");
-    const unsigned nch = pd_gray_segment_chunks(N, chunk_log);
-    if (nch == 0) return fail(PD_EINVAL, "N=%u is too small for walk segments of 2^%u steps", N, chunk_log);
-    const unsigned end = c_end ? c_end : nch;
-    if (c_begin >= end || end > nch) return fail(PD_EINVAL, "walk chunk range outside [0, %u)", nch);
-    if (!part_out) {
-        if (int rc = check_xrange(N, x0, x_count, run_bits, out, layout)) return rc;
-    } else if (x_count == 0 || (x_count & (x_count - 1)) || x0 % x_count || x0 + x_count > (1ull << N)) {
-        return fail(PD_EINVAL, "X-mask range must be an aligned power-of-two block inside [0, 2^N)");
-    }
-    const double2* d = reinterpret_cast<const double2*>(diag);
-    double2* o = reinterpret_cast<double2*>(out);
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    cudaError_t e = pdb::launch_gray_segment(d, N, x0, x_count, c_begin, c_end,
-                                             reinterpret_cast<const double2*>(part_in),
-                                             reinterpret_cast<double2*>(part_out), run_bits, o,
-                                             layout, s, chunk_log);
-    // the last segment: X-masks with an inf or NaN on their diagonal, the reference's products
-    if (e == cudaSuccess && !part_out)
-        e = pdb::launch_nonfinite_fixup(d, false, N, x0, x_count,
-                                        pdb::make_outmap(o, N, run_bits, layout), nullptr, s);
-    if (e != cudaSuccess) return cuda_fail(e, "gray segment launch");
     return PD_OK;
 }
 

@@ -189,6 +189,8 @@ bool gray_share_ok(unsigned N, unsigned run_bits) { return N >= 9 && run_bits <=
 
 uint64_t gray_share_c_min_xmasks(unsigned N) {
     if (N < 13) return ~0ull;
+    static const char* min_env = std::getenv("PD_K2SC_MIN");  // measurement override
+    if (min_env) return std::strtoull(min_env, nullptr, 10);
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {

@@ -168,20 +168,12 @@ uint64_t gray_xmask_grid(unsigned N, uint64_t x_count) {
 // row x_l of D's tile as tile[x_l ^ c][c] gives coalesced writes too. Bank
 // pattern of the permuted read: lanes c and c' hit the same banks only if
 // c = c' mod 8, i.e. the 4 wavefronts a 512 B LDS.128 needs anyway.
-//
-// Output layout. Row-major (diag[(x - x0) 2^N + i]) is the tiled layout with one X-mask block
-// and one column block. The NCCL pipeline of the sharding layer (sharding.py) instead asks for
-// blocks of 2^xb_log X-masks x 2^cb_log columns, each contiguous (X-mask-major inside), ordered
-// X-mask block first: element (xl, i) at ((((xl >> xb_log) 2^(N - cb_log) + (i >> cb_log))
-// 2^xb_log + xl mod 2^xb_log) 2^cb_log + i mod 2^cb_log), so one (rank, walk chunk) piece of the
-// diagonals is one contiguous message.
 
 constexpr int kK1Threads = 256;
 
 __global__ void __launch_bounds__(kK1Threads)
     diag_gather_kernel(const double2* __restrict__ G, unsigned N, uint64_t x0, unsigned t_log,
-                       uint64_t col_blocks_log, uint64_t cb_begin, double2* __restrict__ diag,
-                       unsigned xb_log, unsigned cb_log) {
+                       uint64_t col_blocks_log, uint64_t cb_begin, double2* __restrict__ diag) {
     __shared__ double2 tile[32 * 32];
     const unsigned T = 1u << t_log;
     const uint64_t dim = 1ull << N;
@@ -198,32 +190,19 @@ __global__ void __launch_bounds__(kK1Threads)
     __syncthreads();
     for (unsigned e = threadIdx.x; e < elems; e += kK1Threads) {
         const unsigned xl = e >> t_log, c = e & (T - 1);
-        const uint64_t x = (xb << t_log) + xl, i = (cb << t_log) + c;
-        const uint64_t blk = ((x >> xb_log) << (N - cb_log)) + (i >> cb_log);
-        const uint64_t at = (((blk << xb_log) | (x & ((1ull << xb_log) - 1))) << cb_log) |
-                            (i & ((1ull << cb_log) - 1));
-        diag[at] = tile[(xl ^ c) * T + c];
+        diag[((xb << t_log) + xl) * dim + (cb << t_log) + c] = tile[(xl ^ c) * T + c];
     }
-}
-
-cudaError_t launch_diag_gather_tiled(const double2* G, unsigned N, uint64_t x0, uint64_t x_count,
-                                     uint64_t col0, uint64_t cols, unsigned xb_log, unsigned cb_log,
-                                     double2* diag, cudaStream_t stream) {
-    unsigned t_log = N < 5 ? N : 5;
-    while ((1ull << t_log) > x_count || (1ull << t_log) > cols || t_log > xb_log || t_log > cb_log)
-        --t_log;  // powers of two; a 2^t tile stays inside one output block
-    const uint64_t col_blocks_log = 63 - __builtin_clzll(cols >> t_log);
-    const uint64_t grid = (x_count >> t_log) << col_blocks_log;
-    diag_gather_kernel<<<static_cast<unsigned>(grid), kK1Threads, 0, stream>>>(
-        G, N, x0, t_log, col_blocks_log, col0 >> t_log, diag, xb_log, cb_log);
-    return count_launch();
 }
 
 cudaError_t launch_diag_gather_cols(const double2* G, unsigned N, uint64_t x0, uint64_t x_count,
                                     uint64_t col0, uint64_t cols, double2* diag, cudaStream_t stream) {
-    // row-major: one X-mask block (of x_count, a power of two) and one column block
-    return launch_diag_gather_tiled(G, N, x0, x_count, col0, cols,
-                                    static_cast<unsigned>(__builtin_ctzll(x_count)), N, diag, stream);
+    unsigned t_log = N < 5 ? N : 5;
+    while ((1ull << t_log) > x_count || (1ull << t_log) > cols) --t_log;  // powers of two
+    const uint64_t col_blocks_log = 63 - __builtin_clzll(cols >> t_log);
+    const uint64_t grid = (x_count >> t_log) << col_blocks_log;
+    diag_gather_kernel<<<static_cast<unsigned>(grid), kK1Threads, 0, stream>>>(
+        G, N, x0, t_log, col_blocks_log, col0 >> t_log, diag);
+    return count_launch();
 }
 
 cudaError_t launch_diag_gather(const double2* G, unsigned N, uint64_t x0, uint64_t x_count,

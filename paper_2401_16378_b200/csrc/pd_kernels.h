@@ -21,11 +21,6 @@ cudaError_t launch_diag_gather(const double2* G, unsigned N, uint64_t x0, uint64
 // K1 restricted to the columns [col0, col0 + cols) (a power-of-two aligned range)
 cudaError_t launch_diag_gather_cols(const double2* G, unsigned N, uint64_t x0, uint64_t x_count,
                                     uint64_t col0, uint64_t cols, double2* diag, cudaStream_t stream);
-// K1 into the tiled layout (pd_diag_gather_tiled_device): blocks of 2^xb_log X-masks x 2^cb_log
-// columns, each contiguous
-cudaError_t launch_diag_gather_tiled(const double2* G, unsigned N, uint64_t x0, uint64_t x_count,
-                                     uint64_t col0, uint64_t cols, unsigned xb_log, unsigned cb_log,
-                                     double2* diag, cudaStream_t stream);
 // dst[dst_off[k] + j] = src[src_off[k] + j] for j < run_len, k < count (offsets in elements)
 cudaError_t launch_copy_runs(const double2* src, double2* dst, uint64_t run_len,
                              const uint64_t* src_off, const uint64_t* dst_off, uint64_t count,

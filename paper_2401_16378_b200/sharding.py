@@ -12,14 +12,13 @@ X-masks, which is what makes the device work independent and uniform:
 Data paths, same result bit for bit:
 
 ``mode="nccl"`` (the north star's NCCL replication and gather, pipelined; ``NcclPipeline``):
-  rank g reads only the diagonals of its X-masks, i.e. the tiles (t ^ g, t) of G — 1/P of it.
-  Rank 0 gathers every rank's diagonals (K1) one walk chunk of columns at a time, in walk
-  order, into a tiled buffer where each (rank, chunk) piece is contiguous, and sends each rank
-  its piece with NCCL while it gathers the next chunk. A rank walks each chunk as it arrives
-  (walk segments chained through raw partial sums, bit-identical to one launch, as in the host
-  pipeline of pd_api.cu), finishes its X-masks in sub-blocks, and sends each finished
-  sub-block's coefficients to rank 0 (one NCCL message, unpacked into their places by a run
-  copy kernel) while the next sub-block computes. Gray path, N >= 12.
+  rank g reads only the diagonals of its own X-masks (the tiles (t ^ g, t) of G, 1/P of it),
+  so instead of replicating all of G, rank 0 gathers them (K1, row-major: one contiguous
+  message per rank) one X-mask block at a time and sends each rank its rows with NCCL while it
+  gathers the next block. A rank walks each block as soon as its rows are in (the whole-walk
+  kernel, K2s / K2s-c) and sends each finished block's coefficients to rank 0 (one NCCL message,
+  unpacked into their places by a run copy kernel) while the next block computes. Only the
+  first block's transfer and the last block's gather are exposed. Gray path.
 
 ``mode="nccl-serial"``: one NCCL broadcast of G from rank 0, K1 + K2 on the rank's block,
   grouped NCCL send/recv of the runs straight into rank 0's output (also the WHT path and
@@ -137,7 +136,7 @@ class ShardedDecomposer:
     def __init__(self, num_qubits: int, device: torch.device, group=None,
                  compute: Optional[ShardCompute] = None, path: str = "gray", mode: str = "nccl",
                  mapper=None, buffers: bool = True, pipeline_ops=None,
-                 pipeline_chunk_log: Optional[int] = None, pipeline_sub_bits: Optional[int] = None):
+                 pipeline_blocks: Optional[List[int]] = None):
         if mode not in ("nccl", "nccl-serial", "peer"):
             raise ValueError("mode must be 'nccl', 'nccl-serial' or 'peer'")
         self.group = group
@@ -151,14 +150,13 @@ class ShardedDecomposer:
         self._peer_key = None      # identity of rank 0's (G, out) currently exported / mapped
         self._peer_msg = None      # rank 0: the published handles
         self._peer_bufs = None     # other ranks: (G, out) of rank 0, mapped
-        # mode "nccl": the pipelined schedule where it applies (Gray path, >= 4 walk chunks),
-        # else the serial broadcast / compute / gather ("nccl-serial")
+        # mode "nccl": the pipelined schedule on the Gray path, else the serial broadcast /
+        # compute / gather ("nccl-serial")
         self.pipeline = None
         if mode == "nccl" and path == "gray" and world > 1 and buffers and \
                 (device.type == "cuda" or pipeline_ops is not None):
             try:
-                self.pipeline = NcclPipeline(p, device, group, ops=pipeline_ops,
-                                             chunk_log=pipeline_chunk_log, sub_bits=pipeline_sub_bits)
+                self.pipeline = NcclPipeline(p, device, group, ops=pipeline_ops, sizes=pipeline_blocks)
             except ValueError:
                 self.pipeline = None
         self.mode = "nccl" if self.pipeline is not None else ("peer" if mode == "peer" else "nccl-serial")
@@ -270,26 +268,6 @@ class ShardedDecomposer:
 # Pipelined NCCL mode
 
 
-def gray(k: int) -> int:
-    return k ^ (k >> 1)
-
-
-def walk_segments(nch: int, ones: int = 4, runlen: int = 2) -> List[int]:
-    """Chunk boundaries of the walk segments (decompose_host, pd_api.cu): the first half of the
-    walk in `ones` single chunks, then aligned runs of `runlen`, so that the walk follows the
-    arriving chunks; the second half (the expensive one: the most live chains) is one final
-    segment per sub-block."""
-    bnd, c, half = [0], 0, nch // 2
-    while c < half:
-        L = 1 if len(bnd) - 1 < ones else runlen
-        while L > 1 and (c % L or c + L > half):
-            L >>= 1
-        c += L
-        bnd.append(c)
-    bnd.append(nch)
-    return bnd
-
-
 class TorchP2P:
     """Point-to-point transfers of the pipeline through torch.distributed (NCCL on GPUs: issued
     on the current stream's position, which then waits for them; gloo on CPU: blocking)."""
@@ -342,22 +320,12 @@ class DeviceOps:
     def _s(self, name: str) -> int:
         return self.streams[name].cuda_stream
 
-    def segment_chunks(self, N: int, chunk_log: int) -> int:
-        return int(_ext.device.gray_segment_chunks(N, chunk_log))
+    def gather(self, st, N, G, x0, x_count, out):
+        _ext.device.diag_gather(N, _ptr(G), x0, x_count, _ptr(out), self._s(st))
 
-    def gather_tiled(self, st, N, G, x0, x_count, col0, cols, xb_log, cb_log, out):
-        _ext.device.diag_gather_tiled(N, _ptr(G), x0, x_count, col0, cols, xb_log, cb_log,
-                                      _ptr(out), self._s(st))
-
-    def place_cols(self, st, N, packed, x_count, col0, cols, diag):
-        _ext.device.place_cols(N, _ptr(packed), x_count, col0, cols, _ptr(diag), self._s(st))
-
-    def segment(self, st, N, diag, x0, x_count, chunk_log, c0, c1, part_in, part_out, run_bits,
-                out, layout):
-        _ext.device.gray_segment(N, _ptr(diag), x0, x_count, chunk_log, c0, c1,
-                                 _ptr(part_in) if part_in is not None else 0,
-                                 _ptr(part_out) if part_out is not None else 0, run_bits,
-                                 _ptr(out) if out is not None else 0, layout, self._s(st))
+    def coeffs(self, st, N, diag, x0, x_count, run_bits, out, layout):
+        _ext.device.xmask_coeffs(N, _ptr(diag), x0, x_count, run_bits, _ptr(out), layout, "gray",
+                                 self._s(st))
 
     def copy_runs(self, st, src, dst, run_len, src_off, dst_off):
         _ext.device.copy_runs(_ptr(src), _ptr(dst), run_len, _ptr(src_off), _ptr(dst_off),
@@ -367,134 +335,133 @@ class DeviceOps:
         return torch.tensor(values, dtype=torch.int64, device=self.device)
 
 
-class NcclPipeline:
-    """One rank's share of a full decomposition in the pipelined NCCL mode (module docstring).
+def xmask_blocks(B: int, sizes: Optional[List[int]] = None) -> List[Tuple[int, int]]:
+    """A rank's B X-masks as aligned power-of-two blocks (offset, size), the pipeline's units.
+    Default (profiles/r02_pipeline.md): blocks of 2048 when a rank has >= 4096 X-masks (K2s-c
+    launches: N=14 on 2 or 4 GPUs); else small first and last blocks around larger middle ones
+    (N=14 on 8 GPUs: 256, 256, 512, 512, 256, 256), so that only a small block's transfer is
+    exposed at either end of the step."""
+    if sizes is None:
+        if B >= 4096:
+            sizes = [2048] * (B // 2048)
+        elif B >= 1024:
+            sizes = [B // 8, B // 8, B // 4, B // 4, B // 8, B // 8]
+        else:
+            sizes = [B // 2, B // 2] if B >= 64 else [B]
+    out, off = [], 0
+    for sz in sizes:
+        if sz <= 0 or sz & (sz - 1) or off % sz:
+            raise ValueError("X-mask blocks must be aligned powers of two")
+        out.append((off, sz))
+        off += sz
+    if off != B:
+        raise ValueError("X-mask blocks must cover the rank's X-masks")
+    return out
 
-    Per step (streams: "prod" rank 0's gathers, "comm" NCCL and its copies, "walk"/"walk2"):
-      rank 0, chunk k in walk order (columns gray(k) C .. + C): K1 of every rank's X-masks into
-        the tiled send buffer, its own piece copied into its diagonals, the others' pieces sent
-        (one NCCL group per chunk);
-      rank g: receive chunk k, copy it into its diagonals' columns;
-      every rank: walk segments over the first half as chunks arrive (raw partial sums), then
-        the final segment per sub-block of 2^(N-p-q) X-masks: rank 0 writes its coefficients in
-        place, the others into their run buffer, pack the sub-block's 2^(p+q) runs into one
-        message and send it; rank 0 receives every rank's sub-block and unpacks its runs into
-        their offsets (pd_run_offset) of the output.
+
+class NcclPipeline:
+    """One rank's share of a full decomposition in the pipelined NCCL mode, X-mask blocks.
+
+    Per step, for each block j of the rank's X-masks (streams: "prod" rank 0's gathers, "comm"
+    NCCL and its copies, "walk"/"walk2" alternating):
+      rank 0: K1 of block j of every rank (row-major diagonals, contiguous per rank) and one NCCL
+        group sending each rank its rows; its own rows are its diagonals;
+      rank g: receive block j's rows straight into its diagonals;
+      every rank: the whole walk of block j (K2s / K2s-c + non-finite fixup) as soon as its rows
+        are in; rank 0 stores in place, the others into their run buffer, pack the block's
+        2^(p+q) runs into one message and send it; rank 0 receives every rank's block j and
+        unpacks its runs into their offsets (pd_run_offset) of the output.
+    Exposed per step: the first block's transfer and the last block's gather.
     """
 
-    CHUNK_LOG = 10  # walk chunks of 1024 steps (the host pipeline's; 1/16 of the walk at N=14)
-
-    def __init__(self, plan: ShardPlan, device, group=None, ops=None, chunk_log: Optional[int] = None,
-                 sub_bits: Optional[int] = None, transport=None):
+    def __init__(self, plan: ShardPlan, device, group=None, ops=None, transport=None,
+                 sizes: Optional[List[int]] = None):
         self.plan = plan
         self.transport = transport or TorchP2P(group)
         self.ops = ops or DeviceOps(device)
         N, P, p, B = plan.num_qubits, plan.world, plan.run_bits, plan.x_count
-        self.chunk_log = self.CHUNK_LOG if chunk_log is None else chunk_log
-        self.nch = self.ops.segment_chunks(N, self.chunk_log)
-        if P < 2 or self.nch < 4:
-            raise ValueError("the NCCL pipeline needs >= 2 ranks and >= 4 walk chunks")
-        self.C = 1 << self.chunk_log
-        self.bnd = walk_segments(self.nch)
-        # sub-blocks of >= 256 X-masks (the host pipeline's final launches are 512 at N=14)
-        self.q = (2 if B >= 1024 else (1 if B >= 256 else 0)) if sub_bits is None else sub_bits
-        if (B >> self.q) < 1 or p + self.q > 8:
-            raise ValueError("sub-block bits out of range")
-        self.Q = 1 << self.q
-        self.Bs = B >> self.q                           # X-masks per sub-block
-        self.L = 1 << (2 * (N - p - self.q))            # coefficients per sub-block run
-        self.sub_len = self.L << (p + self.q)           # coefficients per sub-block
+        if P < 2:
+            raise ValueError("the NCCL pipeline needs >= 2 ranks")
+        self.blocks = xmask_blocks(B, sizes)
         dim = 1 << N
         cdt = torch.complex128
         dev = device
-        self.diag = torch.empty(B * dim, dtype=cdt, device=dev)
-        self.part = torch.empty(B * dim, dtype=cdt, device=dev)
-        nruns = 1 << (p + self.q)
+        low = (1 << (2 * (N - p))) - 1
+        self.meta = []  # per block: (bits, run_len L, coefficients)
+        for off, sz in self.blocks:
+            bits = p + (B // sz).bit_length() - 1
+            self.meta.append((bits, 1 << (2 * (N - bits)), sz << N))
+        max_out = max(m[2] for m in self.meta)
         if plan.rank == 0:
-            self.send = torch.empty(dim * dim, dtype=cdt, device=dev)
-            self.gstage = [torch.empty((P - 1) * self.sub_len, dtype=cdt, device=dev) for _ in range(2)]
-            # unpack: run R of rank r's sub-block s (packed at R L) -> pd_run_offset(N, p+q, rQ+s, R)
-            self.unpack_src = self.ops.offsets([R * self.L for R in range(nruns)])
-            self.unpack_dst = {(r, s): self.ops.offsets(
-                [run_offset(N, p + self.q, r * self.Q + s, R) for R in range(nruns)])
-                for r in range(1, P) for s in range(self.Q)}
+            self.send = torch.empty(dim * dim, dtype=cdt, device=dev)  # every rank's diagonals
+            self.gstage = [torch.empty((P - 1) * max_out, dtype=cdt, device=dev) for _ in range(2)]
+            self.unpack_src, self.unpack_dst = [], {}
+            for j, (off, sz) in enumerate(self.blocks):
+                bits, L, _ = self.meta[j]
+                self.unpack_src.append(self.ops.offsets([R * L for R in range(1 << bits)]))
+                for r in range(1, P):
+                    shard = (r * B + off) // sz
+                    self.unpack_dst[(r, j)] = self.ops.offsets(
+                        [run_offset(N, bits, shard, R) for R in range(1 << bits)])
         else:
-            self.stage = [torch.empty(B * self.C, dtype=cdt, device=dev) for _ in range(2)]
+            self.diag = torch.empty(B * dim, dtype=cdt, device=dev)
             self.local = torch.empty(plan.run_len << p, dtype=cdt, device=dev)
-            self.sendsub = [torch.empty(self.sub_len, dtype=cdt, device=dev) for _ in range(2)]
-            # pack: run R = (r, u) of sub-block s, inside the rank's run r at the low 2(N-p)
-            # digits of its global offset -> R L of the message
-            low = (1 << (2 * (N - p))) - 1
-            self.pack_src = {s: self.ops.offsets(
-                [(R >> self.q) * plan.run_len + (run_offset(N, p + self.q, plan.rank * self.Q + s, R) & low)
-                 for R in range(nruns)]) for s in range(self.Q)}
-            self.pack_dst = self.ops.offsets([R * self.L for R in range(nruns)])
-
-    # the send buffer's piece for (rank, column block b): tiled layout, rank block first
-    def _piece(self, rank: int, b: int) -> torch.Tensor:
-        B, C, nb = self.plan.x_count, self.C, self.nch
-        o = (rank * nb + b) * B * C
-        return self.send[o:o + B * C]
-
+            self.sendsub = [torch.empty(max_out, dtype=cdt, device=dev) for _ in range(2)]
+            self.pack_src, self.pack_dst = [], []
+            for j, (off, sz) in enumerate(self.blocks):
+                bits, L, _ = self.meta[j]
+                shard = (plan.rank * B + off) // sz
+                self.pack_src.append(self.ops.offsets(
+                    [(R >> (bits - p)) * plan.run_len + (run_offset(N, bits, shard, R) & low)
+                     for R in range(1 << bits)]))
+                self.pack_dst.append(self.ops.offsets([R * L for R in range(1 << bits)]))
 
     def __call__(self, G: torch.Tensor, out: Optional[torch.Tensor]) -> None:
         plan, ops = self.plan, self.ops
         N, P, p, B = plan.num_qubits, plan.world, plan.run_bits, plan.x_count
-        C, nch, bnd = self.C, self.nch, self.bnd
         dim = 1 << N
-        xb_log = N - p
         ops.begin()
         ready = []
-        # ---- diagonals in, walk order
-        for k in range(nch):
-            b = gray(k)
+        # ---- diagonals in, block by block
+        for off, sz in self.blocks:
             if plan.rank == 0:
-                ops.gather_tiled("prod", N, G, 0, dim, b * C, C, xb_log, self.chunk_log, self.send)
-                ops.place_cols("prod", N, self._piece(0, b), B, b * C, C, self.diag)
+                for r in range(P):
+                    x = r * B + off
+                    ops.gather("prod", N, G, x, sz, self.send[x * dim:(x + sz) * dim])
                 ev = ops.record("prod")
                 ready.append(ev)
                 ops.wait("comm", ev)
                 with ops.on("comm"):
-                    self.transport.exchange([("send", self._piece(r, b), r) for r in range(1, P)])
-            else:
-                st = self.stage[k % 2]
-                with ops.on("comm"):
-                    self.transport.exchange([("recv", st, 0)])
-                ops.place_cols("comm", N, st, B, b * C, C, self.diag)
-                ready.append(ops.record("comm"))
-        # ---- first half of the walk, segment by segment as the chunks arrive
-        for sg in range(len(bnd) - 2):
-            ops.wait("walk", ready[bnd[sg + 1] - 1])
-            ops.segment("walk", N, self.diag, plan.x0, B, self.chunk_log, bnd[sg], bnd[sg + 1],
-                        self.part if sg else None, self.part, 0, None, "global")
-        ops.wait("walk", ready[nch - 1])
-        ops.wait("walk2", ops.record("walk"))
-        # ---- final segments per sub-block; each finished sub-block goes to rank 0
-        done = []
-        for s in range(self.Q):
-            st = "walk" if s % 2 == 0 else "walk2"
-            xs = plan.x0 + s * self.Bs
-            d0 = s * self.Bs * dim
-            if plan.rank == 0:
-                ops.segment(st, N, self.diag[d0:], xs, self.Bs, self.chunk_log, bnd[-2], 0,
-                            self.part[d0:], None, 0, out, "global")
-            else:
-                ops.segment(st, N, self.diag[d0:], xs, self.Bs, self.chunk_log, bnd[-2], 0,
-                            self.part[d0:], None, p, self.local, "runs")
-            done.append(ops.record(st))
-        for s in range(self.Q):
-            ops.wait("comm", done[s])
-            if plan.rank == 0:
-                slot = self.gstage[s % 2]
-                with ops.on("comm"):
-                    self.transport.exchange([("recv", slot[(r - 1) * self.sub_len:r * self.sub_len], r)
+                    self.transport.exchange([("send", self.send[(r * B + off) * dim:(r * B + off + sz) * dim], r)
                                              for r in range(1, P)])
-                for r in range(1, P):
-                    ops.copy_runs("comm", slot[(r - 1) * self.sub_len:], out, self.L, self.unpack_src,
-                                  self.unpack_dst[(r, s)])
             else:
-                buf = self.sendsub[s % 2]
-                ops.copy_runs("comm", self.local, buf, self.L, self.pack_src[s], self.pack_dst)
+                with ops.on("comm"):
+                    self.transport.exchange([("recv", self.diag[off * dim:(off + sz) * dim], 0)])
+                ready.append(ops.record("comm"))
+        # ---- the whole walk of each block as soon as its rows are in
+        done = []
+        for j, (off, sz) in enumerate(self.blocks):
+            st = "walk" if j % 2 == 0 else "walk2"
+            ops.wait(st, ready[j])
+            if plan.rank == 0:
+                ops.coeffs(st, N, self.send[off * dim:], off, sz, 0, out, "global")
+            else:
+                ops.coeffs(st, N, self.diag[off * dim:], plan.x0 + off, sz, p, self.local, "runs")
+            done.append(ops.record(st))
+        # ---- finished blocks to rank 0
+        for j, (off, sz) in enumerate(self.blocks):
+            bits, L, n_out = self.meta[j]
+            ops.wait("comm", done[j])
+            if plan.rank == 0:
+                slot = self.gstage[j % 2]
+                with ops.on("comm"):
+                    self.transport.exchange([("recv", slot[(r - 1) * n_out:r * n_out], r) for r in range(1, P)])
+                for r in range(1, P):
+                    ops.copy_runs("comm", slot[(r - 1) * n_out:], out, L, self.unpack_src[j],
+                                  self.unpack_dst[(r, j)])
+            else:
+                buf = self.sendsub[j % 2][:n_out]
+                ops.copy_runs("comm", self.local, buf, L, self.pack_src[j], self.pack_dst[j])
                 with ops.on("comm"):
                     self.transport.exchange([("send", buf, 0)])
         ops.end()

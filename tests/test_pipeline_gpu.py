@@ -4,9 +4,9 @@ Every rank of a P-rank run executes here as a host thread with its own streams a
 the one GPU; the NCCL transfers are replaced by a loopback transport that hands a finished
 buffer from one thread to another (the sender synchronises its stream first, so no kernel ever
 waits on another rank's kernel). What runs on the device is exactly what each rank of a real
-run executes: rank 0's tiled K1 per walk chunk, the chunk placement, the walk segments chained
-through raw partial sums, the final segments per sub-block in both output layouts, and the run
-packing / unpacking. The assembled output must equal the one-shot decomposition bit for bit.
+run executes: rank 0's K1 per X-mask block of every rank, the per-block walks (K2s / K2s-c and
+the non-finite fixup) in both output layouts, and the run packing / unpacking. The assembled
+output must equal the one-shot decomposition bit for bit.
 """
 import queue
 import threading
@@ -38,13 +38,13 @@ class LoopbackTransport:
                 torch.cuda.current_stream().synchronize()
 
 
-def run_emulated(pd, nq, world, G, sub_bits=None):
+def run_emulated(pd, nq, world, G, blocks=None):
     import torch
     from paper_2401_16378_b200.sharding import NcclPipeline, ShardPlan
     dev = G.device
     out = torch.full((4**nq,), complex(np.nan, np.nan), dtype=torch.complex128, device=dev)
     queues = {(a, b): queue.Queue() for a in range(world) for b in range(world)}
-    pipes = [NcclPipeline(ShardPlan(nq, world, r), dev, sub_bits=sub_bits,
+    pipes = [NcclPipeline(ShardPlan(nq, world, r), dev, sizes=blocks,
                           transport=LoopbackTransport(r, queues)) for r in range(world)]
     errors = []
 
@@ -82,7 +82,7 @@ def test_nccl_pipeline_dataflow_bit_exact(pd, cuda, nq, world):
 
 def test_nccl_pipeline_nonfinite_and_sub_blocks(pd, cuda, port):
     """an inf and a NaN on two ranks' diagonals: the final segments' fixup recomputes those
-    X-masks with the reference's products, in both output layouts; every sub-block split"""
+    X-masks with the reference's products, in both output layouts; several block plans"""
     import torch
     nq, world = 12, 4
     gh = port.random_matrix(nq, 1212)
@@ -92,9 +92,9 @@ def test_nccl_pipeline_nonfinite_and_sub_blocks(pd, cuda, port):
     from oracle import oracle as O
     ns = O.xmask_sample_indices(nq, [100, 3000])
     want_bad = port.coeff_batch(gh, ns)
-    for sub_bits in (0, 1, 2):
-        out = run_emulated(pd, nq, world, G, sub_bits=sub_bits).cpu().numpy()
-        assert same_or_both_nan(out[ns.astype(np.int64)], want_bad), sub_bits
+    for blocks in (None, [1024], [256, 256, 512], [128, 128, 256, 256, 128, 128]):
+        out = run_emulated(pd, nq, world, G, blocks=blocks).cpu().numpy()
+        assert same_or_both_nan(out[ns.astype(np.int64)], want_bad), blocks
         ok = np.ones(4**nq, dtype=bool)
         ok[ns.astype(np.int64)] = False
         sample = np.flatnonzero(ok)[::997]

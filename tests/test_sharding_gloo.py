@@ -133,9 +133,9 @@ def test_plan_rejects_bad_world_sizes():
 
 # ---------------------------------------------------------------------------------------------
 # the pipelined NCCL mode's schedule (sharding.NcclPipeline) with numpy stand-ins of its device
-# primitives: which diagonal pieces go to which rank in which order, the segment chaining and the
-# sub-block packing / unpacking of the runs. The stand-in walk sums in a different order (a
-# matrix product), so results are compared to the oracle within 1e-12.
+# primitives: which diagonal rows go to which rank in which order, the per-block walks in both
+# output layouts and the block packing / unpacking of the runs. The stand-in walk sums in a
+# different order (a matrix product), so results are compared to the oracle within 1e-12.
 
 class CpuPipelineOps:
     """numpy restatements of the pipeline's device primitives (include/pd_api.h)"""
@@ -156,41 +156,21 @@ class CpuPipelineOps:
     def wait(self, name, ev):
         pass
 
-    def segment_chunks(self, N, chunk_log):
-        return (1 << N) >> chunk_log if chunk_log < N else 0
-
-    def gather_tiled(self, st, N, G, x0, x_count, col0, cols, xb_log, cb_log, out):
+    def gather(self, st, N, G, x0, x_count, out):  # K1: out[(x - x0) 2^N + i] = G[i ^ x][i]
         dim = 1 << N
         g = G.reshape(dim, dim).numpy()
-        o = out.numpy()
-        xl = np.arange(x_count, dtype=np.int64)[:, None]
-        i = np.arange(col0, col0 + cols, dtype=np.int64)[None, :]
-        blk = ((xl >> xb_log) << (N - cb_log)) + (i >> cb_log)
-        at = (((blk << xb_log) | (xl & ((1 << xb_log) - 1))) << cb_log) | (i & ((1 << cb_log) - 1))
-        o[at] = g[i ^ (x0 + xl), i]
+        i = np.arange(dim, dtype=np.int64)[None, :]
+        x = np.arange(x0, x0 + x_count, dtype=np.int64)[:, None]
+        out.numpy()[:x_count * dim] = g[i ^ x, i].reshape(-1)
 
-    def place_cols(self, st, N, packed, x_count, col0, cols, diag):
-        dim = 1 << N
-        d = diag.numpy()[:x_count * dim].reshape(x_count, dim)
-        d[:, col0:col0 + cols] = packed.numpy()[:x_count * cols].reshape(x_count, cols)
-
-    def segment(self, st, N, diag, x0, x_count, chunk_log, c0, c1, part_in, part_out, run_bits, out,
-                layout):
+    def coeffs(self, st, N, diag, x0, x_count, run_bits, out, layout):
         from oracle import oracle as O
         dim = 1 << N
-        C = 1 << chunk_log
-        c1 = c1 or dim // C
-        ks = np.arange(c0 * C, c1 * C, dtype=np.int64)
+        ks = np.arange(dim, dtype=np.int64)
         gk = ks ^ (ks >> 1)
         z = np.arange(dim, dtype=np.int64)
         sign = 1.0 - 2.0 * (np.bitwise_count(gk[:, None] & z[None, :]) & 1)
-        D = diag.numpy()[:x_count * dim].reshape(x_count, dim)
-        S = D[:, gk] @ sign
-        if part_in is not None:
-            S = S + part_in.numpy()[:x_count * dim].reshape(x_count, dim)
-        if part_out is not None:
-            part_out.numpy()[:x_count * dim] = S.reshape(-1)
-            return
+        S = diag.numpy()[:x_count * dim].reshape(x_count, dim)[:, gk] @ sign
         o = out.numpy()
         low = 2 * (N - run_bits)
         for xl in range(x_count):
@@ -210,7 +190,7 @@ class CpuPipelineOps:
         return torch.tensor(values, dtype=torch.int64)
 
 
-def _pipeline_worker(rank, world, port, nq, chunk_log, sub_bits, result_path):
+def _pipeline_worker(rank, world, port, nq, blocks, result_path):
     import sys
     sys.path.insert(0, ROOT)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -225,7 +205,7 @@ def _pipeline_worker(rank, world, port, nq, chunk_log, sub_bits, result_path):
         G = torch.full((dim, dim), complex(np.nan, np.nan), dtype=torch.complex128)  # never read
         out = None
     sd = ShardedDecomposer(nq, torch.device("cpu"), mode="nccl", pipeline_ops=CpuPipelineOps(),
-                           pipeline_chunk_log=chunk_log, pipeline_sub_bits=sub_bits)
+                           pipeline_blocks=blocks)
     assert sd.mode == "nccl" and sd.pipeline is not None
     for _ in range(2):
         sd(G, out)
@@ -235,11 +215,11 @@ def _pipeline_worker(rank, world, port, nq, chunk_log, sub_bits, result_path):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,nq,chunk_log,sub_bits", [(2, 6, 2, 2), (4, 6, 2, 1), (8, 7, 3, 1),
-                                                         (4, 8, 4, 2)])
-def test_nccl_pipeline_schedule_matches_oracle(tmp_path, world, nq, chunk_log, sub_bits):
+@pytest.mark.parametrize("world,nq,blocks", [(2, 6, None), (4, 6, [2, 2, 4, 4, 2, 2]), (8, 7, None),
+                                             (4, 8, [8, 8, 16, 16, 8, 8]), (2, 8, [128])])
+def test_nccl_pipeline_schedule_matches_oracle(tmp_path, world, nq, blocks):
     result = str(tmp_path / "out.npy")
-    mp.start_processes(_pipeline_worker, args=(world, _free_port(), nq, chunk_log, sub_bits, result),
+    mp.start_processes(_pipeline_worker, args=(world, _free_port(), nq, blocks, result),
                        nprocs=world, join=True, start_method="spawn")
     got = np.load(result)
     import sys
@@ -250,10 +230,16 @@ def test_nccl_pipeline_schedule_matches_oracle(tmp_path, world, nq, chunk_log, s
     assert np.max(np.abs(got - want)) <= 1e-12 * np.max(np.abs(want))
 
 
-def test_walk_segments_cover_the_walk():
-    from paper_2401_16378_b200.sharding import walk_segments
-    for nch in (4, 8, 16, 32, 64):
-        b = walk_segments(nch)
-        assert b[0] == 0 and b[-1] == nch and b[-2] == nch // 2
-        assert all(x < y for x, y in zip(b, b[1:]))
-        assert b[1:5] == [1, 2, 3, 4][:len(b[1:5])] or nch < 8
+def test_xmask_blocks_plans():
+    from paper_2401_16378_b200.sharding import xmask_blocks
+    assert xmask_blocks(2048) == [(0, 256), (256, 256), (512, 512), (1024, 512), (1536, 256), (1792, 256)]
+    assert xmask_blocks(8192) == [(0, 2048), (2048, 2048), (4096, 2048), (6144, 2048)]
+    assert xmask_blocks(512) == [(0, 256), (256, 256)]
+    for B in (1, 2, 16, 64, 1024, 4096):
+        blocks = xmask_blocks(B)
+        assert sum(sz for _, sz in blocks) == B
+        assert all(off % sz == 0 for off, sz in blocks)
+    with pytest.raises(ValueError):
+        xmask_blocks(64, [16, 32, 16])   # 32 at offset 16 is not aligned
+    with pytest.raises(ValueError):
+        xmask_blocks(64, [32])
