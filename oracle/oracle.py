@@ -177,7 +177,7 @@ class Reference:
     def _check(self, rc: int) -> None:
         if rc != 0:
             msg = self.lib.pdref_last_error().decode()
-            raise (ValueError if rc in (-1, -2) else RuntimeError)(msg)
+            raise (ValueError if rc in (-1, -2, -4) else RuntimeError)(msg)
 
     class Matrix:
         def __init__(self, ref: "Reference", handle: int, nq: int):

@@ -9,7 +9,7 @@
 // Every entry point forwards to the reference's public C++ API
 // (proj/include/paulidecomp/decompose.hpp:33-56, bench.hpp, matrix.hpp) and maps
 // its exceptions to status codes: -1 invalid_argument, -2 length_error,
-// -3 anything else (message in pdref_last_error()).
+// -4 FormatError, -3 anything else (message in pdref_last_error()).
 #include <algorithm>
 #include <complex>
 #include <cstdint>
@@ -41,6 +41,9 @@ int guarded(F&& f) {
     } catch (const std::length_error& e) {
         g_error = e.what();
         return -2;
+    } catch (const FormatError& e) {
+        g_error = e.what();
+        return -4;
     } catch (const std::exception& e) {
         g_error = e.what();
         return -3;

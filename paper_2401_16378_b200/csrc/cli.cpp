@@ -4,7 +4,6 @@
 //                    [--serial] [--path gray|wht]
 //   pdb200 recompose --in CSV [--out PATH] [--format text|binary]
 //   pdb200 coeff LABEL --in PATH [--format text|binary]
-//   pdb200 bench [--n-min N] [--n-max N] [--reps R] [--seed S] [--threads T] [--out PATH]
 //
 // Paths may be "-" (stdin/stdout). Exit codes follow main.cpp:140-158: 0 success, 1 usage or
 // format error, 2 resource or internal error. `decompose` prints "N=… nonzero=… seconds=…" to
@@ -18,7 +17,6 @@
 #include <string>
 #include <vector>
 
-#include "paulidecomp_b200/bench.hpp"
 #include "paulidecomp_b200/decompose.hpp"
 #include "paulidecomp_b200/io.hpp"
 
@@ -31,24 +29,16 @@ struct Args {
     double eps = 0.0;
     unsigned threads = 1;
     bool serial = false, have_in = false;
-    BenchOptions bench;
 };
 
 [[noreturn]] void usage(const std::string& why) { throw std::invalid_argument(why); }
 
 Args parse(int argc, char** argv) {
     Args a;
-    if (argc < 2) usage("a subcommand is required: decompose, recompose, coeff or bench");
+    if (argc < 2) usage("a subcommand is required: decompose, recompose or coeff");
     a.cmd = argv[1];
-    if (a.cmd != "decompose" && a.cmd != "recompose" && a.cmd != "coeff" && a.cmd != "bench")
+    if (a.cmd != "decompose" && a.cmd != "recompose" && a.cmd != "coeff")
         usage("unknown subcommand \"" + a.cmd + "\"");
-    auto positive = [](const std::string& opt, const std::string& v) {
-        unsigned long long x = 0;
-        std::size_t used = 0;
-        try { x = std::stoull(v, &used); } catch (...) { usage(opt + " needs a number"); }
-        if (used != v.size()) usage(opt + " needs a number");
-        return x;
-    };
     for (int k = 2; k < argc; ++k) {
         const std::string s = argv[k];
         auto value = [&]() -> std::string {
@@ -70,20 +60,13 @@ Args parse(int argc, char** argv) {
             try { a.threads = static_cast<unsigned>(std::stoul(v)); } catch (...) { usage("--threads needs a number"); }
             if (a.threads == 0) usage("--threads must be positive");
         } else if (s == "--serial" && a.cmd == "decompose") a.serial = true;
-        else if (a.cmd == "bench" && (s == "--n-min" || s == "--n-max" || s == "--reps" || s == "--threads")) {
-            const unsigned long long v = positive(s, value());
-            if (v == 0) usage(s + " must be positive");
-            unsigned& dst = s == "--n-min" ? a.bench.n_min : s == "--n-max" ? a.bench.n_max
-                          : s == "--reps" ? a.bench.reps : a.bench.threads;
-            dst = static_cast<unsigned>(v);
-        } else if (a.cmd == "bench" && s == "--seed") a.bench.seed = positive(s, value());
         else if (s == "--path" && a.cmd == "decompose") {
             a.path = value();
             if (a.path != "gray" && a.path != "wht") usage("--path must be gray or wht");
         } else if (a.cmd == "coeff" && a.label.empty() && !s.empty() && s[0] != '-') a.label = s;
         else usage("unexpected argument \"" + s + "\"");
     }
-    if (!a.have_in && a.cmd != "bench") usage("--in is required");
+    if (!a.have_in) usage("--in is required");
     if (a.cmd == "coeff" && a.label.empty()) usage("coeff needs an operator label");
     return a;
 }
@@ -91,17 +74,6 @@ Args parse(int argc, char** argv) {
 MatrixFormat fmt(const Args& a) { return a.format == "binary" ? MatrixFormat::binary : MatrixFormat::text; }
 
 int run(const Args& a) {
-    if (a.cmd == "bench") {  // main.cpp:110-128, bench.cpp:141-150
-        const std::vector<BenchRecord> records = run_bench(a.bench);
-        if (a.out == "-") {
-            write_bench_csv(records, std::cout);
-        } else {
-            std::ofstream f(a.out);
-            if (!f) throw std::invalid_argument("cannot open " + a.out + " for writing");
-            write_bench_csv(records, f);
-        }
-        return 0;
-    }
     if (a.cmd == "decompose") {
         const auto t0 = std::chrono::steady_clock::now();
         unsigned N = 0;

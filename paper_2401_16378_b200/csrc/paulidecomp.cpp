@@ -11,6 +11,7 @@
 #include <new>
 #include <string>
 #include <unordered_map>
+#include <utility>
 
 #include "pd_api.h"
 
@@ -197,6 +198,15 @@ Complex coeff_slow(const DenseMatrix& g, std::uint64_t n, MultCount& count) {
 
 Complex oracle_coeff_kron(const DenseMatrix& g, std::uint64_t n) {
     return oracle_coeff_view(g.data(), g.num_qubits(), n);
+}
+
+// bench.cpp:42-46: the per-(N, rep) seed is one splitmix64 output of the mixed master seed
+std::uint64_t matrix_seed(std::uint64_t seed, unsigned num_qubits, unsigned rep) {
+    std::uint64_t z = (seed ^ (std::uint64_t{num_qubits} * 0xD6E8FEB86659FD93ull) ^
+                       (std::uint64_t{rep} * 0xCA5A826395121157ull)) + 0x9E3779B97F4A7C15ull;
+    for (const auto& [shift, mul] : {std::pair{30, 0xBF58476D1CE4E5B9ull}, std::pair{27, 0x94D049BB133111EBull}})
+        z = (z ^ (z >> shift)) * mul;
+    return z ^ (z >> 31);
 }
 
 DenseMatrix random_matrix(unsigned num_qubits, std::uint64_t seed) {  // bench.cpp:48-58, on the GPU
