@@ -410,7 +410,7 @@ def run_ours(args) -> None:
             line["wht_path"]["roofline"]["frac"] = (line["wht_path"]["roofline"]["achieved"]
                                                     / line["wht_path"]["roofline"]["peak"])
         if world == 1 and rank == 0:
-            line["side_configs"] = side_configs(pd, dev, stream, sptr, peaks)
+            line["side_configs"] = side_configs(pd, dev, stream, sptr, peaks, not args.no_cpu_baseline)
 
     # ---- e2e through the public API with pinned host buffers (H2D + D2H inside)
     if not args.no_e2e:
@@ -437,7 +437,59 @@ def k2_dadd(nq):
     return 2.0 * 8.0**nq
 
 
-def side_configs(pd, dev, stream, sptr, peaks):
+def host_e2e(pd, g, steps, path="gray"):
+    """pd.decompose on host buffers, wall clock per call after one warm-up: pinned in and out
+    (`e2e`, the bench contract's form), and the reference binding's normal call on a plain numpy
+    array returning a new array (`pageable`, bindings/module.cpp:21-42)."""
+    import numpy as np
+    import torch
+    nq = g.shape[0].bit_length() - 1
+    gp_t = torch.empty(g.shape, dtype=torch.complex128, pin_memory=True)
+    op_t = torch.empty(4**nq, dtype=torch.complex128, pin_memory=True)
+    gp, op = gp_t.numpy(), op_t.numpy()
+    gp[...] = g
+    gpage = np.array(g, copy=True)
+
+    def clock(fn):
+        fn()
+        t = []
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            fn()
+            t.append(time.perf_counter() - t0)
+        return sum(t) / len(t)
+
+    pinned = clock(lambda: pd.decompose(gp, out=op, path=path))
+    page_new = clock(lambda: pd.decompose(gpage, path=path))
+    nbytes = 16 * 4**nq
+    return {"value": 4**nq / pinned, "unit": UNIT, "ms_per_step": pinned * 1e3,
+            "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+            "api": "decompose(pinned numpy, out=pinned numpy)",
+            "pageable": {"value": 4**nq / page_new, "unit": UNIT, "ms_per_step": page_new * 1e3,
+                         "api": "decompose(numpy array) -> new numpy array (pageable in and out)"}}
+
+
+def n12_cpu_baseline(g, gpu_out):
+    """BASELINE configs[3] on the host: the reference's own decompose_parallel
+    (proj/src/decompose.cpp:95-131, 205-211) over all 4^12 coefficients on every hardware
+    thread, once, timed with a wall clock like bench.cpp:105-108; its output must equal the
+    GPU's bit for bit."""
+    import numpy as np
+    from oracle import oracle as O
+    ref = O.reference()
+    if ref is None:
+        return {"unavailable": "oracle/_ref not built"}
+    h = ref.matrix(g)
+    t0 = time.perf_counter()
+    c = ref.decompose(h, threads=ref.cores)
+    sec = time.perf_counter() - t0
+    return {"value": c.size / sec, "unit": UNIT, "cores": ref.cores, "kind": "reference",
+            "sample": "full N=12 decomposition (16,777,216 coefficients) via reference "
+                      "decompose_parallel (proj/src, -O3), one run", "seconds": sec,
+            "matches_gpu_full_array": bool(np.array_equal(c, gpu_out))}
+
+
+def side_configs(pd, dev, stream, sptr, peaks, cpu_n12=True):
     """The other BASELINE configs on one GPU, device-resident, CUDA events, 3 warm-ups:
     configs[3] (full N=12 decomposition, the metric's other size), configs[1] (65,536 batched
     single strings at N=10), configs[2] (full N=10 Hermitian) and configs[0] (full N=6)."""
@@ -469,6 +521,10 @@ def side_configs(pd, dev, stream, sptr, peaks):
     res["n12_full_gray"] = {"config": "BASELINE configs[3]: full N=12, N(0,1) complex128",
                             "value": 4**nq / (ms / 1e3), "unit": UNIT, "ms_per_step": ms,
                             "fp64_frac_incl_k1": dadd / (ms / 1e3) / peak}
+    # the same matrix through the public API from host memory, pinned and pageable
+    res["n12_full_gray"]["e2e"] = host_e2e(pd, g.cpu().numpy(), 10)
+    if cpu_n12:
+        res["n12_full_gray"]["cpu_baseline"] = n12_cpu_baseline(g.cpu().numpy(), out.cpu().numpy())
     nq = 10
     g = torch.empty((2**nq, 2**nq), dtype=torch.complex128, device=dev)
     g.copy_(torch.from_numpy(gen.standard_normal((2**nq, 2**nq)) + 1j * gen.standard_normal((2**nq, 2**nq))))
@@ -504,36 +560,48 @@ def run_e2e(args, pd, plan, G, out, dev, stream, barrier, max_over_ranks, world,
     broadcast/compute/gather, rank 0 downloads the coefficients."""
     import torch
 
+    import numpy as np
     nq = args.qubits
     nbytes = 16 * 4**nq
     steps = max(1, min(args.steps, 5))
     if world == 1:
+        def clock(fn):
+            fn()  # warm-up: the context allocates its buffers (and staging slots)
+            t = []
+            for _ in range(steps):
+                t0 = time.perf_counter()
+                r = fn()
+                t.append(time.perf_counter() - t0)
+                del r
+            return sum(t) / len(t)
+
+        def entry(per, api):
+            return {"value": 4**nq / per, "unit": UNIT, "ms_per_step": per * 1e3,
+                    "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "api": api}
+
+        wht = args.path == "gray" and not args.no_extras
         gh_t = torch.empty(G.shape, dtype=torch.complex128, pin_memory=True)
         gh_t.copy_(G)
         oh_t = torch.empty(4**nq, dtype=torch.complex128, pin_memory=True)
         gh, oh = gh_t.numpy(), oh_t.numpy()
-        pd.decompose(gh, out=oh, path=args.path)  # warm-up: the context allocates its buffers
-        times = []
-        for _ in range(steps):
-            t0 = time.perf_counter()
-            pd.decompose(gh, out=oh, path=args.path)
-            times.append(time.perf_counter() - t0)
-        per = sum(times) / len(times)
-        res = {"value": 4**nq / per, "unit": UNIT, "h2d_bytes_per_step": nbytes,
-               "d2h_bytes_per_step": nbytes, "ms_per_step": per * 1e3,
-               "api": "paper_2401_16378_b200.decompose(pinned numpy, out=pinned numpy)"}
-        if args.path == "gray" and not args.no_extras:
+        res = entry(clock(lambda: pd.decompose(gh, out=oh, path=args.path)),
+                    "paper_2401_16378_b200.decompose(pinned numpy, out=pinned numpy)")
+        if wht:
             # the separately reported WHT path through the same call (per-block tile uploads
             # overlapping the downloads)
-            pd.decompose(gh, out=oh, path="wht")
-            wt = []
-            for _ in range(steps):
-                t0 = time.perf_counter()
-                pd.decompose(gh, out=oh, path="wht")
-                wt.append(time.perf_counter() - t0)
-            wper = sum(wt) / len(wt)
-            res["wht_path_e2e"] = {"value": 4**nq / wper, "unit": UNIT, "ms_per_step": wper * 1e3,
-                                   "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes}
+            res["wht_path_e2e"] = entry(clock(lambda: pd.decompose(gh, out=oh, path="wht")),
+                                        "decompose(pinned numpy, out=pinned numpy, path='wht')")
+        # the reference binding's normal call: a plain (pageable) numpy matrix in, a new numpy
+        # array out (bindings/module.cpp:21-42), served through the pinned slot rings of
+        # csrc/pd_stage.cu
+        gpage = np.array(gh, copy=True)
+        del gh, oh, gh_t, oh_t
+        res["pageable"] = entry(clock(lambda: pd.decompose(gpage, path=args.path)),
+                                "paper_2401_16378_b200.decompose(numpy array) -> new numpy array")
+        if wht:
+            res["wht_path_e2e"]["pageable"] = entry(
+                clock(lambda: pd.decompose(gpage, path="wht")),
+                "decompose(numpy array, path='wht') -> new numpy array")
         return res
     from paper_2401_16378_b200.sharding import ShardedDecomposer
     if sd is None:

@@ -95,6 +95,15 @@ PauliDecomposition decompose_serial_quaternary(const DenseMatrix& g, MultCount& 
 
 DenseMatrix recompose(const PauliDecomposition& d);
 
+// ---- bits.hpp / pauli.hpp helpers (bits.hpp:17-26, pauli.hpp:16-20) ----
+constexpr std::uint64_t pow2(unsigned exponent) { return std::uint64_t{1} << exponent; }
+constexpr std::uint64_t pow4(unsigned exponent) { return std::uint64_t{1} << (2 * exponent); }
+enum class PauliOp : unsigned { I = 0, X = 1, Y = 2, Z = 3 };
+// operator at position t of tensor number n (base-4 digit t, digit 0 rightmost in labels)
+constexpr PauliOp pauli_digit(std::uint64_t n, unsigned t) {
+    return static_cast<PauliOp>((n >> (2 * t)) & 3u);
+}
+
 // ---- pauli_string.hpp (label <-> tensor number) ----
 std::uint64_t string_to_index(std::string_view label, unsigned num_qubits);
 std::string index_to_string(std::uint64_t n, unsigned num_qubits);

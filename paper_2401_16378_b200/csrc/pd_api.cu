@@ -16,12 +16,14 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <utility>
 #include <vector>
 
 #include "pd_api.h"
 #include "pd_device.cuh"
 #include "pd_kernels.h"
+#include "pd_stage.h"
 
 
 namespace {
@@ -133,6 +135,7 @@ struct pd_ctx {
     std::vector<pd_ctx*> subs;       // multi-device context: one sub-context per listed device
     void* stage = nullptr;           // pinned host staging (single-string diagonal)
     size_t stage_bytes = 0;
+    pdb::Stager* stager = nullptr;   // pinned slot rings for pageable caller buffers (pd_stage.h)
 
     int ensure(void** p, size_t* have, size_t need) {
         if (*have >= need) return PD_OK;
@@ -159,6 +162,27 @@ int bind(pd_ctx* ctx) {
     if (!ctx) return fail(PD_EINVAL, "null context");
     PD_CUDA(cudaSetDevice(ctx->device));
     return PD_OK;
+}
+
+// A failed host-buffer call returns only once every stream of the context (and of its
+// sub-contexts) is idle: copies and kernels queued before the failure may still read the
+// caller's g or write its out, and the next call would reuse ctx->g/out/part under them. The
+// first error's code and message are what the caller sees.
+int drained(pd_ctx* ctx, int rc) {
+    if (rc == PD_OK || !ctx) return rc;
+    const std::string msg = t_error;
+    std::vector<pd_ctx*> all{ctx};
+    all.insert(all.end(), ctx->subs.begin(), ctx->subs.end());
+    for (pd_ctx* c : all) {
+        if (cudaSetDevice(c->device) != cudaSuccess) continue;
+        for (cudaStream_t s : {c->stream, c->stream2, c->d2h, c->h2d, c->gather})
+            if (s) cudaStreamSynchronize(s);
+        if (c->stager) c->stager->finish();  // host scatters into the caller's out
+    }
+    cudaSetDevice(ctx->device);
+    cudaGetLastError();
+    t_error = msg;
+    return rc;
 }
 
 }  // namespace
@@ -233,6 +257,8 @@ int pd_ctx_destroy(pd_ctx* ctx) {
     cudaSetDevice(ctx->device);
     for (cudaStream_t s : {ctx->stream, ctx->stream2, ctx->d2h, ctx->h2d, ctx->gather})
         if (s) cudaStreamSynchronize(s);
+    delete ctx->stager;
+    ctx->stager = nullptr;
     for (void* p : {ctx->g, ctx->out, ctx->scratch, ctx->ns, ctx->part, ctx->sel_tiles, ctx->sel_idx,
                     ctx->sel_val})
         if (p) cudaFree(p);
@@ -458,12 +484,23 @@ int pd_decompose(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_path 
     if (int rc = check_qubits(N)) return rc;
     if (int rc = bind(ctx)) return rc;
     if (!g || !out) return fail(PD_EINVAL, "null buffer");
-    if (ctx->subs.size() > 1) return decompose_multi(ctx, N, g, out, path);
-    return decompose_host(ctx, N, g, out, path);
+    if (ctx->subs.size() > 1) return drained(ctx, decompose_multi(ctx, N, g, out, path));
+    return drained(ctx, decompose_host(ctx, N, g, out, path));
+}
+
+namespace {
+int decompose_sparse(pd_ctx* ctx, unsigned N, const double* g, pd_path path, double threshold,
+                     int check_finite, uint64_t* n_kept);
 }
 
 int pd_decompose_sparse(pd_ctx* ctx, unsigned N, const double* g, pd_path path, double threshold,
                         int check_finite, uint64_t* n_kept) {
+    return drained(ctx, decompose_sparse(ctx, N, g, path, threshold, check_finite, n_kept));
+}
+
+namespace {
+int decompose_sparse(pd_ctx* ctx, unsigned N, const double* g, pd_path path, double threshold,
+                     int check_finite, uint64_t* n_kept) {
     if (int rc = check_qubits(N)) return rc;
     if (int rc = bind(ctx)) return rc;
     if (!g || !n_kept) return fail(PD_EINVAL, "null buffer");
@@ -505,6 +542,7 @@ int pd_decompose_sparse(pd_ctx* ctx, unsigned N, const double* g, pd_path path, 
     *n_kept = kept;
     return PD_OK;
 }
+}  // namespace
 
 int pd_sparse_fetch(pd_ctx* ctx, uint64_t* idx, double* vals) {
     if (int rc = bind(ctx)) return rc;
@@ -569,9 +607,71 @@ struct HostTimeline {
     }
 };
 
+// the pinned slot rings of pd_stage.h, created on the first pageable call (PD_STAGE_SLOT_MB,
+// PD_STAGE_WORKERS override the slot size and the worker count)
+int stager_of(pd_ctx* ctx, pdb::Stager** out) {
+    if (!ctx->stager) {
+        const char* mb = std::getenv("PD_STAGE_SLOT_MB");
+        const char* wk = std::getenv("PD_STAGE_WORKERS");
+        const size_t slot = (mb ? std::max(1, std::atoi(mb)) : 32) * (size_t{1} << 20);
+        const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
+        const unsigned workers = wk ? static_cast<unsigned>(std::atoi(wk)) : std::min(12u, hw - 2);
+        ctx->stager = new pdb::Stager(ctx->device, slot, 4, 16, workers);
+        if (!ctx->stager->ok()) {
+            delete ctx->stager;
+            ctx->stager = nullptr;
+            return fail(PD_ENOMEM, "cannot allocate the pinned staging slots");
+        }
+    }
+    *out = ctx->stager;
+    return PD_OK;
+}
+
+// Host <-> device copies of one host-buffer call: straight DMA for page-locked buffers, the
+// pinned slot rings (pd_stage.h) for pageable ones, decided per buffer.
+struct HostXfer {
+    pdb::Stager* st = nullptr;
+    bool up_staged = false, down_staged = false;
+
+    int init(pd_ctx* ctx, const void* g, const void* out) {
+        up_staged = g && pdb::host_pageable(g);
+        down_staged = out && pdb::host_pageable(out);
+        if (up_staged || down_staged) return stager_of(ctx, &st);
+        return PD_OK;
+    }
+    int up2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height,
+             cudaStream_t s) {
+        const cudaError_t e = up_staged ? st->upload_2d(dst, dpitch, src, spitch, width, height, s)
+                                        : cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height,
+                                                            cudaMemcpyHostToDevice, s);
+        return e == cudaSuccess ? PD_OK : cuda_fail(e, "host upload");
+    }
+    int up(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+        return up2d(dst, bytes, src, bytes, bytes, 1, s);
+    }
+    // D2H once `after` (may be null) has fired
+    int down(void* dst, const void* src, size_t bytes, cudaEvent_t after, cudaStream_t s) {
+        cudaError_t e = cudaSuccess;
+        if (down_staged) {
+            e = st->download(dst, src, bytes, after, s);
+        } else {
+            if (after) e = cudaStreamWaitEvent(s, after, 0);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s);
+        }
+        return e == cudaSuccess ? PD_OK : cuda_fail(e, "host download");
+    }
+    // every staged download landed in the caller's buffer
+    int finish() {
+        const cudaError_t e = st ? st->finish() : cudaSuccess;
+        return e == cudaSuccess ? PD_OK : cuda_fail(e, "host download");
+    }
+};
+
 // the host-buffer decomposition; out == nullptr leaves the coefficients in ctx->out
 int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_path path) {
     const size_t bytes = elems(N) * sizeof(double2);
+    HostXfer xf;
+    if (int rc = xf.init(ctx, g, out)) return rc;
     if (int rc = ctx->ensure(&ctx->g, &ctx->g_bytes, bytes)) return rc;
     if (int rc = ctx->ensure(&ctx->out, &ctx->out_bytes, bytes)) return rc;
     const uint64_t sb = pd_scratch_bytes(N, 1ull << N, path);
@@ -584,12 +684,15 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
             PD_CUDA(cudaMemGetInfo(&free_b, &total_b));
             const size_t want = free_b > (1ull << 30) ? free_b - (1ull << 30) : 0;  // 1 GiB margin
             if (int rc = ctx->ensure(&ctx->scratch, &ctx->scratch_bytes, want)) return rc;
-            if (int rc = upload(ctx, ctx->g, g, bytes)) return rc;
+            if (int rc = xf.up(ctx->g, g, bytes, ctx->stream)) return rc;
             if (int rc = pd_decompose_device_blocked(N, static_cast<const double*>(ctx->g),
                                                      static_cast<double*>(ctx->out), ctx->scratch,
                                                      ctx->scratch_bytes, path, ctx->stream))
                 return rc;
-            if (out) PD_CUDA(cudaMemcpyAsync(out, ctx->out, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+            if (out) {
+                if (int rc = xf.down(out, ctx->out, bytes, nullptr, ctx->stream)) return rc;
+            }
+            if (int rc = xf.finish()) return rc;
             PD_CUDA(cudaStreamSynchronize(ctx->stream));
             // the scratch took all but 1 GiB of the device: give it back rather than keep it cached
             PD_CUDA(cudaFree(ctx->scratch));
@@ -600,12 +703,15 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
     }
     const uint64_t dim = 1ull << N;
     if (path == PD_PATH_NAIVE || N < 10) {
-        if (int rc = upload(ctx, ctx->g, g, bytes)) return rc;
+        if (int rc = xf.up(ctx->g, g, bytes, ctx->stream)) return rc;
         if (int rc = pd_decompose_device(N, static_cast<const double*>(ctx->g),
                                          static_cast<double*>(ctx->out), ctx->scratch, path,
                                          ctx->stream))
             return rc;
-        if (out) PD_CUDA(cudaMemcpyAsync(out, ctx->out, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+        if (out) {
+            if (int rc = xf.down(out, ctx->out, bytes, nullptr, ctx->stream)) return rc;
+        }
+        if (int rc = xf.finish()) return rc;
         PD_CUDA(cudaStreamSynchronize(ctx->stream));
         return PD_OK;
     }
@@ -639,19 +745,21 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
     const unsigned nblk = 1u << kBits;
     // the coefficients of the X-masks whose top `bits` bits equal xt: 2^bits runs of
     // 4^(N - bits), one per value of z's top bits (pd_run_offset); event slot ev
-    auto download_bits = [&](unsigned bits, uint64_t xt, unsigned ev, cudaStream_t s) -> int {
-        PD_CUDA(cudaEventRecord(ctx->block_done[ev], s));
-        PD_CUDA(cudaStreamWaitEvent(ctx->d2h, ctx->block_done[ev], 0));
+    // (block_done[ev] must have been recorded after the block's kernels)
+    auto download_bits = [&](unsigned bits, uint64_t xt, unsigned ev) -> int {
         const uint64_t len = 1ull << (2 * (N - bits));
         for (uint64_t r = 0; out && r < (1ull << bits); ++r) {
             const uint64_t off = 2 * pd_run_offset(N, bits, xt, r);
-            PD_CUDA(cudaMemcpyAsync(out + off, dout + off, len * sizeof(double2),
-                                    cudaMemcpyDeviceToHost, ctx->d2h));
+            if (int rc = xf.down(out + off, dout + off, len * sizeof(double2),
+                                 r == 0 ? ctx->block_done[ev] : nullptr, ctx->d2h))
+                return rc;
         }
+        if (!out) PD_CUDA(cudaStreamWaitEvent(ctx->d2h, ctx->block_done[ev], 0));
         return PD_OK;
     };
     auto download = [&](unsigned q, cudaStream_t s) -> int {  // block q's runs, once computed
-        return download_bits(kBits, q, q, s);
+        PD_CUDA(cudaEventRecord(ctx->block_done[q], s));
+        return download_bits(kBits, q, q);
     };
     // the walk segments keep raw partial sums of every coefficient (one more G-sized buffer);
     // without room for them, upload G whole and walk in one launch per download block
@@ -701,9 +809,9 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
             const uint64_t L = bnd[sg + 1] - bnd[sg];
             const uint64_t gb = bnd[sg] ^ (bnd[sg] >> 1);
             const uint64_t col0 = (gb & ~(L - 1)) * C, W = L * C;
-            PD_CUDA(cudaMemcpy2DAsync(gdev + 2 * col0, dim * sizeof(double2), g + 2 * col0,
-                                      dim * sizeof(double2), W * sizeof(double2), dim,
-                                      cudaMemcpyHostToDevice, ctx->h2d));
+            if (int rc = xf.up2d(gdev + 2 * col0, dim * sizeof(double2), g + 2 * col0,
+                                 dim * sizeof(double2), W * sizeof(double2), dim, ctx->h2d))
+                return rc;
             PD_CUDA(cudaEventRecord(ctx->copied[sg], ctx->h2d));
             tl.mark("up" + std::to_string(sg), ctx->h2d);
             PD_CUDA(cudaStreamWaitEvent(ctx->gather, ctx->copied[sg], 0));
@@ -712,18 +820,19 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
                                                          reinterpret_cast<double2*>(diag), ctx->gather);
             if (e != cudaSuccess) return cuda_fail(e, "diag_gather launch");
             PD_CUDA(cudaEventRecord(ctx->cols_ready[sg], ctx->gather));
+            // the walk segment over these columns is queued at once: with a pageable g the
+            // next upload holds this thread while its slots fill
+            if (sg + 1 < nseg) {
+                PD_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->cols_ready[sg], 0));
+                e = pdb::launch_gray_segment(reinterpret_cast<const double2*>(diag), N, 0, dim,
+                                             bnd[sg], bnd[sg + 1], sg ? part : nullptr, part, 0,
+                                             nullptr, PD_LAYOUT_GLOBAL, ctx->stream, kChunkLog);
+                if (e != cudaSuccess) return cuda_fail(e, "gray segment launch");
+                tl.mark("seg" + std::to_string(sg), ctx->stream);
+            }
         }
-        // segments as the columns arrive, then the final segment in download blocks (continuing
-        // from the stored raw sums) over ctx->stream and stream2
-        for (unsigned sg = 0; sg + 1 < nseg; ++sg) {
-            PD_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->cols_ready[sg], 0));
-            cudaError_t e = pdb::launch_gray_segment(reinterpret_cast<const double2*>(diag), N, 0,
-                                                     dim, bnd[sg], bnd[sg + 1],
-                                                     sg ? part : nullptr, part, 0, nullptr,
-                                                     PD_LAYOUT_GLOBAL, ctx->stream, kChunkLog);
-            if (e != cudaSuccess) return cuda_fail(e, "gray segment launch");
-            tl.mark("seg" + std::to_string(sg), ctx->stream);
-        }
+        // then the final segment in download blocks (continuing from the stored raw sums) over
+        // ctx->stream and stream2
         PD_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->cols_ready[nseg - 1], 0));
         PD_CUDA(cudaEventRecord(ctx->seg_done, ctx->stream));
         PD_CUDA(cudaStreamWaitEvent(ctx->stream2, ctx->seg_done, 0));
@@ -736,6 +845,12 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
         if (!tail_env && xc < 512) tail_log = 0;  // N=13 (256-X-mask blocks): 52.5 -> 54.0 ms split
         if (nblk - 1 + (1u << tail_log) > static_cast<unsigned>(pd_ctx::kBlocks)) tail_log = 0;
         unsigned launches = 0;
+        struct Pending {
+            unsigned bits;
+            uint64_t xt;
+            unsigned ev;
+        };
+        std::vector<Pending> pending;  // downloads, queued once every block is launched
         for (unsigned q = 0; q < nblk; ++q) {
             const unsigned sub_log = q + 1 == nblk ? tail_log : 0;
             const uint64_t xs = xc >> sub_log;
@@ -751,10 +866,14 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
                                                     false, N, x0, xs, gmap, nullptr, s);
                 if (e != cudaSuccess) return cuda_fail(e, "gray block launch");
                 tl.mark("blk" + std::to_string(launches), s);
-                if (int rc = download_bits(kBits + sub_log, (uint64_t{q} << sub_log) | sb, launches, s))
-                    return rc;
-                tl.mark("d2h" + std::to_string(launches), ctx->d2h);
+                PD_CUDA(cudaEventRecord(ctx->block_done[launches], s));
+                pending.push_back({kBits + sub_log, (uint64_t{q} << sub_log) | sb, launches});
             }
+        }
+        // (a pageable out can hold this thread until a slot drains: every block is queued first)
+        for (const Pending& d : pending) {
+            if (int rc = download_bits(d.bits, d.xt, d.ev)) return rc;
+            tl.mark("d2h" + std::to_string(d.ev), ctx->d2h);
         }
     } else {
         // WHT: block q's X-masks (top kBits bits = q) read only the tiles (t ^ q, t) of G, so G
@@ -768,7 +887,7 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
         unsigned wht_grp = grp_env ? static_cast<unsigned>(std::atoi(grp_env)) : kWhtGroupLog;
         if (wht_grp > kBits) wht_grp = kBits;
         if (!tiled) {
-            if (int rc = upload(ctx, ctx->g, g, bytes)) return rc;
+            if (int rc = xf.up(ctx->g, g, bytes, ctx->stream)) return rc;
             if (gray && pd_diag_gather_device(N, gdev, 0, dim, diag, ctx->stream)) return PD_ECUDA;
             PD_CUDA(cudaEventRecord(ctx->gathered, ctx->stream));
             PD_CUDA(cudaStreamWaitEvent(ctx->stream2, ctx->gathered, 0));
@@ -785,9 +904,10 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
                     for (uint64_t r = 0; r < nblk; ++r) {
                         const uint64_t c0 = (r ^ q) & ~(gw - 1);
                         const uint64_t off = 2 * ((r * xc) * dim + c0 * xc);
-                        PD_CUDA(cudaMemcpy2DAsync(gdev + off, dim * sizeof(double2), g + off,
-                                                  dim * sizeof(double2), gw * xc * sizeof(double2), xc,
-                                                  cudaMemcpyHostToDevice, ctx->h2d));
+                        if (int rc = xf.up2d(gdev + off, dim * sizeof(double2), g + off,
+                                             dim * sizeof(double2), gw * xc * sizeof(double2), xc,
+                                             ctx->h2d))
+                            return rc;
                     }
                     PD_CUDA(cudaEventRecord(ctx->copied[q], ctx->h2d));
                     tl.mark("up" + std::to_string(q), ctx->h2d);
@@ -812,6 +932,7 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
             if (int rc2 = download(q, s)) return rc2;
         }
     }
+    if (int rc = xf.finish()) return rc;
     PD_CUDA(cudaStreamSynchronize(ctx->d2h));
     PD_CUDA(cudaStreamSynchronize(ctx->stream));
     PD_CUDA(cudaStreamSynchronize(ctx->stream2));
