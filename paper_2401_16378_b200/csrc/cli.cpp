@@ -96,7 +96,17 @@ int run(const Args& a) {
 
 }  // namespace
 
+constexpr const char* kUsage =
+    "usage: pdb200 decompose --in PATH [--out PATH] [--format text|binary] [--eps E] [--threads T]\n"
+    "                        [--serial] [--path gray|wht]\n"
+    "       pdb200 recompose --in CSV [--out PATH] [--format text|binary]\n"
+    "       pdb200 coeff LABEL --in PATH [--format text|binary]\n";
+
 int main(int argc, char** argv) {
+    if (argc == 2 && (std::strcmp(argv[1], "--help") == 0 || std::strcmp(argv[1], "-h") == 0)) {
+        std::cout << kUsage;
+        return 0;
+    }
     try {
         return run(parse(argc, argv));
     } catch (const FormatError& e) {

@@ -1,0 +1,59 @@
+"""The reference's own test suites, run unchanged against the B200 drop-in.
+
+* proj/tests/python/test_smoke.py (9 tests) with `import paulidecomp` resolving to
+  tests/reference_suite/paulidecomp, the reference package's re-export over this package.
+* proj/tests/acceptance.cpp, compiled unmodified against include/compat/paulidecomp/*.hpp and
+  linked with libpaulidecomp_b200.so (oracle/Makefile `suite`). Criteria 1-8 are the
+  library's guarantees and must PASS. Criterion 9 drives the reference CLI's `bench`
+  subcommand and its CSV, the benchmark harness SURVEY.md §2 marks out of scope; our pdb200
+  has no `bench`, so 9 is reported and must fail for exactly that reason.
+
+Both files are copied from /root/reference at build time into the git-ignored oracle/_ref/suite
+(they travel to the GPU box with the snapshot; nothing reads /root/reference at run time)."""
+import os
+import re
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+SUITE = os.path.join(ROOT, "oracle", "_ref", "suite")
+
+
+def suite_file(name):
+    p = os.path.join(SUITE, name)
+    if not os.path.exists(p):
+        pytest.fail(f"{p} missing: build() copies the reference suites when /root/reference exists")
+    return p
+
+
+def test_reference_python_smoke_suite(cuda):
+    smoke = suite_file("test_smoke.py")
+    env = dict(os.environ, PYTHONPATH=os.pathsep.join(
+        [os.path.join(ROOT, "tests", "reference_suite"), ROOT]))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider",
+                        "--rootdir", SUITE, smoke], cwd=SUITE, env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert re.search(r"\b9 passed\b", r.stdout), r.stdout[-2000:]
+    # the suite really ran against this package, not the reference's extension
+    probe = subprocess.run([sys.executable, "-c", "import paulidecomp, paper_2401_16378_b200 as p;"
+                            "print(paulidecomp.decompose is p.decompose)"],
+                           env=env, capture_output=True, text=True, timeout=300)
+    assert probe.stdout.strip() == "True", probe.stderr
+
+
+def test_reference_acceptance_criteria(cuda):
+    exe = suite_file("acceptance_b200")
+    cli = os.path.join(ROOT, "paper_2401_16378_b200", "pdb200")
+    r = subprocess.run([exe, cli], capture_output=True, text=True, timeout=900)
+    status = {int(m.group(2)): m.group(1) for m in re.finditer(r"^(PASS|FAIL) (\d+)/9 ", r.stdout, re.M)}
+    assert sorted(status) == list(range(1, 10)), r.stdout
+    for k in range(1, 9):
+        assert status[k] == "PASS", r.stdout
+    # criterion 9 passes the CLI pipeline and exit-code checks and stops at `pdb200 bench`
+    assert status[9] == "FAIL" and "bench exited nonzero" in r.stdout, r.stdout
