@@ -177,6 +177,26 @@ class CpuBaseline:
         return time.perf_counter() - t0
 
 
+def n12_cpu_baseline(g, gpu_out):
+    """BASELINE configs[3] on the host: the reference's own decompose_parallel
+    (proj/src/decompose.cpp:95-131, 205-211) over all 4^12 coefficients on every hardware
+    thread, once, timed with a wall clock like bench.cpp:105-108; its output must equal the
+    GPU's bit for bit."""
+    import numpy as np
+    from oracle import oracle as O
+    ref = O.reference()
+    if ref is None:
+        return {"unavailable": "oracle/_ref not built"}
+    h = ref.matrix(g)
+    t0 = time.perf_counter()
+    c = ref.decompose(h, threads=ref.cores)
+    sec = time.perf_counter() - t0
+    return {"value": c.size / sec, "unit": UNIT, "cores": ref.cores, "kind": "reference",
+            "sample": "full N=12 decomposition (16,777,216 coefficients) via reference "
+                      "decompose_parallel (proj/src, -O3), one run", "seconds": sec,
+            "matches_gpu_full_array": bool(np.array_equal(c, gpu_out))}
+
+
 def run_reference_arm(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -467,26 +487,6 @@ def host_e2e(pd, g, steps, path="gray"):
             "api": "decompose(pinned numpy, out=pinned numpy)",
             "pageable": {"value": 4**nq / page_new, "unit": UNIT, "ms_per_step": page_new * 1e3,
                          "api": "decompose(numpy array) -> new numpy array (pageable in and out)"}}
-
-
-def n12_cpu_baseline(g, gpu_out):
-    """BASELINE configs[3] on the host: the reference's own decompose_parallel
-    (proj/src/decompose.cpp:95-131, 205-211) over all 4^12 coefficients on every hardware
-    thread, once, timed with a wall clock like bench.cpp:105-108; its output must equal the
-    GPU's bit for bit."""
-    import numpy as np
-    from oracle import oracle as O
-    ref = O.reference()
-    if ref is None:
-        return {"unavailable": "oracle/_ref not built"}
-    h = ref.matrix(g)
-    t0 = time.perf_counter()
-    c = ref.decompose(h, threads=ref.cores)
-    sec = time.perf_counter() - t0
-    return {"value": c.size / sec, "unit": UNIT, "cores": ref.cores, "kind": "reference",
-            "sample": "full N=12 decomposition (16,777,216 coefficients) via reference "
-                      "decompose_parallel (proj/src, -O3), one run", "seconds": sec,
-            "matches_gpu_full_array": bool(np.array_equal(c, gpu_out))}
 
 
 def side_configs(pd, dev, stream, sptr, peaks, cpu_n12=True):
