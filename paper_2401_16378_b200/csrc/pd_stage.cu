@@ -79,6 +79,7 @@ void StagePool::parallel(unsigned parts, const std::function<void(unsigned)>& fn
 
 namespace {
 constexpr size_t kPieceMin = size_t{1} << 20;  // smallest share of a band per thread
+constexpr size_t kHugePage = size_t{2} << 20;
 }
 
 Stager::Stager(int device, size_t slot_bytes, unsigned up_slots, unsigned down_slots, unsigned workers)
@@ -187,12 +188,21 @@ cudaError_t Stager::download(void* dst, const void* src, size_t bytes, cudaEvent
     return cudaSuccess;
 }
 
+// the shares are cut at 2 MiB boundaries of the destination, so that no two threads
+// first-touch the same (transparent huge) page of a fresh output array
 void Stager::scatter(char* dst, const char* src, size_t bytes) {
     const unsigned parts = static_cast<unsigned>(
-        std::max<size_t>(1, std::min<size_t>(pool_.workers() + 1, bytes / kPieceMin)));
+        std::max<size_t>(1, std::min<size_t>(pool_.workers() + 1, bytes / kHugePage)));
+    const uintptr_t d0 = reinterpret_cast<uintptr_t>(dst);
+    auto cut = [&](unsigned k) -> size_t {
+        if (k == 0) return 0;
+        if (k == parts) return bytes;
+        const uintptr_t at = (d0 + bytes * k / parts) & ~(uintptr_t{kHugePage} - 1);
+        return at <= d0 ? 0 : std::min<size_t>(bytes, at - d0);
+    };
     pool_.parallel(parts, [&](unsigned k) {
-        const size_t a = bytes * k / parts, b = bytes * (k + 1) / parts;
-        std::memcpy(dst + a, src + a, b - a);
+        const size_t a = cut(k), b = cut(k + 1);
+        if (b > a) std::memcpy(dst + a, src + a, b - a);
     });
 }
 
