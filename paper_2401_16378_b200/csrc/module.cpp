@@ -13,9 +13,14 @@
 
 #include <sys/mman.h>
 
+#include <algorithm>
+#include <atomic>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "paulidecomp_b200/bench.hpp"
@@ -44,7 +49,8 @@ unsigned matrix_qubits(const ComplexArray& a) {
 py::array_t<Complex> new_result(py::ssize_t count) {
     const size_t bytes = static_cast<size_t>(count) * sizeof(Complex);
     constexpr size_t kHuge = size_t{2} << 20;
-    if (bytes < (size_t{64} << 20)) return py::array_t<Complex>(count);
+    static const char* thp = std::getenv("PD_RESULT_THP");  // "0": a plain numpy array (A/B)
+    if (bytes < (size_t{64} << 20) || (thp && thp[0] == '0')) return py::array_t<Complex>(count);
     const size_t span = ((bytes + kHuge - 1) & ~(kHuge - 1)) + kHuge;
     void* base = mmap(nullptr, span, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
     if (base == MAP_FAILED) return py::array_t<Complex>(count);
@@ -63,6 +69,44 @@ py::array_t<Complex> new_result(py::ssize_t count) {
     return py::array_t<Complex>({count}, {static_cast<py::ssize_t>(sizeof(Complex))},
                                 reinterpret_cast<Complex*>(data), owner);
 }
+
+// Populates (allocates and zeroes, content untouched) the pages of a fresh result array on
+// helper threads while the decomposition runs: MADV_POPULATE_WRITE leaves pages that are
+// already present alone, so it cannot race with the staging threads' writes. Without it the
+// first touch of 4 GiB happened inside the staging scatter, behind the GPU.
+class Prefault {
+public:
+    Prefault(void* data, size_t bytes, unsigned threads) {
+#ifdef MADV_POPULATE_WRITE
+        constexpr uintptr_t kPage = 4096;
+        const uintptr_t b = (reinterpret_cast<uintptr_t>(data) + kPage - 1) & ~(kPage - 1);
+        const uintptr_t e = (reinterpret_cast<uintptr_t>(data) + bytes) & ~(kPage - 1);
+        if (e <= b) return;
+        begin_ = b;
+        end_ = e;
+        for (unsigned k = 0; k < threads; ++k)
+            pool_.emplace_back([this] {
+                constexpr uintptr_t kPiece = uintptr_t{32} << 20;
+                for (;;) {
+                    const uintptr_t at = begin_ + next_.fetch_add(kPiece);
+                    if (at >= end_) return;
+                    const uintptr_t len = std::min(kPiece, end_ - at);
+                    if (madvise(reinterpret_cast<void*>(at), len, MADV_POPULATE_WRITE) != 0) return;
+                }
+            });
+#else
+        (void)data, (void)bytes, (void)threads;
+#endif
+    }
+    ~Prefault() {
+        for (auto& t : pool_) t.join();
+    }
+
+private:
+    uintptr_t begin_ = 0, end_ = 0;
+    std::atomic<uintptr_t> next_{0};
+    std::vector<std::thread> pool_;
+};
 
 Path parse_path(const std::string& s) {
     if (s == "gray") return Path::Gray;
@@ -95,6 +139,12 @@ py::array_t<Complex> py_decompose(const ComplexArray& g, unsigned threads, bool 
     if (!devices.is_none()) devs = devices.cast<std::vector<int>>();
     {
         py::gil_scoped_release nogil;
+        static const char* pf_env = std::getenv("PD_RESULT_PREFAULT");  // threads; "0" = off
+        const unsigned pf = pf_env ? static_cast<unsigned>(std::atoi(pf_env)) : 2u;  // 2-12 threads measured: 2 best (profiles/r02_pageable_probe.txt)
+        const size_t nbytes = static_cast<size_t>(count) * sizeof(Complex);
+        std::unique_ptr<Prefault> prefault;
+        if (out.is_none() && pf && nbytes >= (size_t{64} << 20))
+            prefault = std::make_unique<Prefault>(dst, nbytes, pf);
         if (!devs.empty()) decompose_into(src, N, dst, p, devs);
         else decompose_into(src, N, dst, p);
     }

@@ -20,7 +20,7 @@ bool host_pageable(const void* p) {
 
 struct StagePool::Batch {
     const std::function<void(unsigned)>* fn;
-    std::atomic<unsigned> left;
+    unsigned left;  // guarded by mu
     std::mutex mu;
     std::condition_variable cv;
 };
@@ -50,10 +50,10 @@ void StagePool::loop() {
         }
         Batch* b = job.first;
         (*b->fn)(job.second);
-        if (b->left.fetch_sub(1) == 1) {
-            std::lock_guard<std::mutex> lk(b->mu);
-            b->cv.notify_all();
-        }
+        // decrement under the batch mutex: the caller returns (and destroys the batch) only
+        // after it has seen the count reach 0 under that mutex, i.e. after this block is done
+        std::lock_guard<std::mutex> lk(b->mu);
+        if (--b->left == 0) b->cv.notify_all();
     }
 }
 
@@ -64,7 +64,7 @@ void StagePool::parallel(unsigned parts, const std::function<void(unsigned)>& fn
     }
     Batch b;
     b.fn = &fn;
-    b.left.store(parts - 1);
+    b.left = parts - 1;
     {
         std::lock_guard<std::mutex> lk(mu_);
         for (unsigned k = 1; k < parts; ++k) queue_.emplace_back(&b, k);
@@ -72,14 +72,13 @@ void StagePool::parallel(unsigned parts, const std::function<void(unsigned)>& fn
     cv_.notify_all();
     fn(0);
     std::unique_lock<std::mutex> lk(b.mu);
-    b.cv.wait(lk, [&] { return b.left.load() == 0; });
+    b.cv.wait(lk, [&] { return b.left == 0; });
 }
 
 // ---------------- stager ----------------
 
 namespace {
 constexpr size_t kPieceMin = size_t{1} << 20;  // smallest share of a band per thread
-constexpr size_t kHugePage = size_t{2} << 20;
 }
 
 Stager::Stager(int device, size_t slot_bytes, unsigned up_slots, unsigned down_slots, unsigned workers)
@@ -188,21 +187,12 @@ cudaError_t Stager::download(void* dst, const void* src, size_t bytes, cudaEvent
     return cudaSuccess;
 }
 
-// the shares are cut at 2 MiB boundaries of the destination, so that no two threads
-// first-touch the same (transparent huge) page of a fresh output array
 void Stager::scatter(char* dst, const char* src, size_t bytes) {
     const unsigned parts = static_cast<unsigned>(
-        std::max<size_t>(1, std::min<size_t>(pool_.workers() + 1, bytes / kHugePage)));
-    const uintptr_t d0 = reinterpret_cast<uintptr_t>(dst);
-    auto cut = [&](unsigned k) -> size_t {
-        if (k == 0) return 0;
-        if (k == parts) return bytes;
-        const uintptr_t at = (d0 + bytes * k / parts) & ~(uintptr_t{kHugePage} - 1);
-        return at <= d0 ? 0 : std::min<size_t>(bytes, at - d0);
-    };
+        std::max<size_t>(1, std::min<size_t>(pool_.workers() + 1, bytes / kPieceMin)));
     pool_.parallel(parts, [&](unsigned k) {
-        const size_t a = cut(k), b = cut(k + 1);
-        if (b > a) std::memcpy(dst + a, src + a, b - a);
+        const size_t a = bytes * k / parts, b = bytes * (k + 1) / parts;
+        std::memcpy(dst + a, src + a, b - a);
     });
 }
 
