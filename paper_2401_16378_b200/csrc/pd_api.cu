@@ -660,6 +660,18 @@ struct HostXfer {
         }
         return e == cudaSuccess ? PD_OK : cuda_fail(e, "host download");
     }
+    // several device -> host pieces once `after` has fired (staged: packed into shared slots)
+    int down_pieces(const std::vector<pdb::Stager::Piece>& pieces, cudaEvent_t after, cudaStream_t s) {
+        cudaError_t e = cudaSuccess;
+        if (down_staged) {
+            e = st->download(pieces.data(), pieces.size(), after, s);
+        } else {
+            if (after) e = cudaStreamWaitEvent(s, after, 0);
+            for (size_t i = 0; e == cudaSuccess && i < pieces.size(); ++i)
+                e = cudaMemcpyAsync(pieces[i].dst, pieces[i].src, pieces[i].bytes, cudaMemcpyDeviceToHost, s);
+        }
+        return e == cudaSuccess ? PD_OK : cuda_fail(e, "host download");
+    }
     // every staged download landed in the caller's buffer
     int finish() {
         const cudaError_t e = st ? st->finish() : cudaSuccess;
@@ -746,16 +758,19 @@ int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pat
     // the coefficients of the X-masks whose top `bits` bits equal xt: 2^bits runs of
     // 4^(N - bits), one per value of z's top bits (pd_run_offset); event slot ev
     // (block_done[ev] must have been recorded after the block's kernels)
+    std::vector<pdb::Stager::Piece> pieces;
     auto download_bits = [&](unsigned bits, uint64_t xt, unsigned ev) -> int {
-        const uint64_t len = 1ull << (2 * (N - bits));
-        for (uint64_t r = 0; out && r < (1ull << bits); ++r) {
-            const uint64_t off = 2 * pd_run_offset(N, bits, xt, r);
-            if (int rc = xf.down(out + off, dout + off, len * sizeof(double2),
-                                 r == 0 ? ctx->block_done[ev] : nullptr, ctx->d2h))
-                return rc;
+        if (!out) {
+            PD_CUDA(cudaStreamWaitEvent(ctx->d2h, ctx->block_done[ev], 0));
+            return PD_OK;
         }
-        if (!out) PD_CUDA(cudaStreamWaitEvent(ctx->d2h, ctx->block_done[ev], 0));
-        return PD_OK;
+        const uint64_t len = 1ull << (2 * (N - bits));
+        pieces.clear();
+        for (uint64_t r = 0; r < (1ull << bits); ++r) {
+            const uint64_t off = 2 * pd_run_offset(N, bits, xt, r);
+            pieces.push_back({out + off, dout + off, len * sizeof(double2)});
+        }
+        return xf.down_pieces(pieces, ctx->block_done[ev], ctx->d2h);
     };
     auto download = [&](unsigned q, cudaStream_t s) -> int {  // block q's runs, once computed
         PD_CUDA(cudaEventRecord(ctx->block_done[q], s));

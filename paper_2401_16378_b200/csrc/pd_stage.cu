@@ -162,37 +162,72 @@ cudaError_t Stager::take_down_slot(unsigned* out) {
     return cudaSuccess;
 }
 
-cudaError_t Stager::download(void* dst, const void* src, size_t bytes, cudaEvent_t after,
+cudaError_t Stager::download(const Piece* pieces, size_t count, cudaEvent_t after,
                              cudaStream_t stream) {
     if (after) {
         if (cudaError_t e = cudaStreamWaitEvent(stream, after, 0)) return e;
     }
-    const char* s = static_cast<const char*>(src);
-    char* d = static_cast<char*>(dst);
-    for (size_t off = 0; off < bytes; off += slot_bytes_) {
-        const size_t n = std::min(slot_bytes_, bytes - off);
-        unsigned k = 0;
-        if (cudaError_t e = take_down_slot(&k)) return e;
-        Slot& slot = down_[k];
-        cudaError_t e = cudaMemcpyAsync(slot.host, s + off, n, cudaMemcpyDeviceToHost, stream);
-        if (e == cudaSuccess) e = cudaEventRecord(slot.done, stream);
+    unsigned k = 0;
+    size_t fill = 0;   // bytes of the open slot in use
+    bool open = false;
+    std::vector<Seg> segs;
+    auto close = [&]() -> cudaError_t {
+        if (!open) return cudaSuccess;
+        cudaError_t e = cudaEventRecord(down_[k].done, stream);
         if (e != cudaSuccess) return e;
         {
             std::lock_guard<std::mutex> lk(mu_);
-            slot.busy = true;
-            drains_.push_back({k, d + off, n});
+            down_[k].busy = true;
+            drains_.push_back({k, std::move(segs)});
         }
         cv_.notify_all();
+        segs.clear();
+        open = false;
+        return cudaSuccess;
+    };
+    for (size_t i = 0; i < count; ++i) {
+        const char* s = static_cast<const char*>(pieces[i].src);
+        char* d = static_cast<char*>(pieces[i].dst);
+        for (size_t off = 0; off < pieces[i].bytes;) {
+            if (open && fill == slot_bytes_) {
+                if (cudaError_t e = close()) return e;
+            }
+            if (!open) {
+                if (cudaError_t e = take_down_slot(&k)) return e;
+                open = true;
+                fill = 0;
+            }
+            const size_t n = std::min(slot_bytes_ - fill, pieces[i].bytes - off);
+            if (cudaError_t e = cudaMemcpyAsync(down_[k].host + fill, s + off, n, cudaMemcpyDeviceToHost,
+                                                stream))
+                return e;
+            segs.push_back({d + off, fill, n});
+            fill += n;
+            off += n;
+        }
     }
-    return cudaSuccess;
+    return close();
 }
 
-void Stager::scatter(char* dst, const char* src, size_t bytes) {
+void Stager::scatter(const std::vector<Seg>& segs, const char* slot) {
+    size_t total = 0;
+    for (const Seg& g : segs) total += g.bytes;
     const unsigned parts = static_cast<unsigned>(
-        std::max<size_t>(1, std::min<size_t>(pool_.workers() + 1, bytes / kPieceMin)));
+        std::max<size_t>(1, std::min<size_t>(pool_.workers() + 1, total / kPieceMin)));
     pool_.parallel(parts, [&](unsigned k) {
-        const size_t a = bytes * k / parts, b = bytes * (k + 1) / parts;
-        std::memcpy(dst + a, src + a, b - a);
+        // linear share [a, b) of the slot's bytes, i.e. of the segments laid end to end
+        size_t a = total * k / parts;
+        const size_t b = total * (k + 1) / parts;
+        size_t base = 0;
+        for (const Seg& g : segs) {
+            if (a >= b) break;
+            if (a < base + g.bytes) {
+                const size_t in = a - base, n = std::min(b, base + g.bytes) - a;
+                std::memcpy(g.dst + in, slot + g.off + in, n);
+                a += n;
+            }
+            base += g.bytes;
+        }
     });
 }
 
@@ -204,11 +239,11 @@ void Stager::drain_loop() {
             std::unique_lock<std::mutex> lk(mu_);
             cv_.wait(lk, [&] { return stop_ || !drains_.empty(); });
             if (drains_.empty()) return;
-            job = drains_.front();
+            job = std::move(drains_.front());
         }
         Slot& slot = down_[job.slot];
         const cudaError_t e = cudaEventSynchronize(slot.done);
-        if (e == cudaSuccess) scatter(job.dst, slot.host, job.bytes);
+        if (e == cudaSuccess) scatter(job.segs, slot.host);
         {
             std::lock_guard<std::mutex> lk(mu_);
             if (e != cudaSuccess && drain_error_ == cudaSuccess) drain_error_ = e;

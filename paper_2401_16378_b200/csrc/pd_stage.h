@@ -64,8 +64,18 @@ public:
     }
     // D2H of `bytes` from device src to pageable host dst once `after` (may be null) has fired;
     // the D2H is enqueued on `stream`, the host scatter happens on the drain thread
+    struct Piece {
+        void* dst;
+        const void* src;
+        size_t bytes;
+    };
     cudaError_t download(void* dst, const void* src, size_t bytes, cudaEvent_t after,
-                         cudaStream_t stream);
+                         cudaStream_t stream) {
+        const Piece p{dst, src, bytes};
+        return download(&p, 1, after, stream);
+    }
+    // several pieces packed into the slots back to back (a slot's pieces drain as one job)
+    cudaError_t download(const Piece* pieces, size_t count, cudaEvent_t after, cudaStream_t stream);
     // wait until every download has landed in host memory; the first error seen, if any
     cudaError_t finish();
 
@@ -76,14 +86,18 @@ private:
         bool used = false;
         bool busy = false;           // download slot: waiting for its drain
     };
+    struct Seg {
+        char* dst;
+        size_t off;  // in the slot
+        size_t bytes;
+    };
     struct Drain {
         unsigned slot;
-        char* dst;
-        size_t bytes;
+        std::vector<Seg> segs;
     };
     cudaError_t take_down_slot(unsigned* slot);
     void drain_loop();
-    void scatter(char* dst, const char* src, size_t bytes);
+    void scatter(const std::vector<Seg>& segs, const char* slot);
 
     int device_;
     size_t slot_bytes_;
