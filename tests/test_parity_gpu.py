@@ -699,3 +699,47 @@ def test_serial_quaternary_driver(pd, cuda, golden, nq):
     assert same_values(pd.decompose(g, threads=0, serial=True), golden[f"normal{nq}_serial"])
     with pytest.raises(ValueError):
         pd.decompose(g, threads=0)
+
+
+def test_random_large_sizes_host_buffers(pd, cuda, port):
+    """Hypothesis-drawn N = 12 … 14 through the public API, with the matrix and the result in
+    pageable or page-locked host memory (pinned slot rings vs direct DMA), matrix kinds that
+    stress the sums (N(0,1), small integers: exact partial sums, real, Hermitian), Gray or WHT:
+    4096 seeded coefficients against the oracle (Gray bit for bit, WHT within 1e-11·max|c|)
+    plus Parseval over the whole array."""
+    import torch
+    from hypothesis import HealthCheck, given, settings
+    from hypothesis import strategies as st
+
+    @settings(max_examples=8, deadline=None, suppress_health_check=list(HealthCheck))
+    @given(st.sampled_from([12, 12, 13, 13, 14]), st.sampled_from(["gray", "gray", "wht"]),
+           st.sampled_from(["normal", "integer", "real", "hermitian"]), st.booleans(), st.booleans(),
+           st.integers(0, 2**32 - 1))
+    def check(nq, path, kind, pin_in, pin_out, seed):
+        rng = np.random.default_rng(seed)
+        d = 2**nq
+        g = torch.empty((d, d), dtype=torch.complex128, pin_memory=pin_in).numpy()
+        if kind == "integer":
+            g.real = rng.integers(-4, 5, (d, d))
+            g.imag = rng.integers(-4, 5, (d, d))
+        else:
+            g.real = rng.standard_normal((d, d))
+            g.imag = 0.0 if kind == "real" else rng.standard_normal((d, d))
+            if kind == "hermitian":
+                g[...] = (g + g.conj().T) / 2
+        out = torch.empty(4**nq, dtype=torch.complex128, pin_memory=True).numpy() if pin_out else \
+            np.empty(4**nq, dtype=np.complex128)
+        out[...] = np.nan
+        pd.decompose(g, path=path, out=out)
+        ns = np.sort(rng.choice(4**nq, 4096, replace=False)).astype(np.uint64)
+        want = port.coeff_batch(g, ns)
+        got = out[ns.astype(np.int64)]
+        if path == "gray":
+            assert same_values(got, want)
+        else:
+            assert np.max(np.abs(got - want)) <= 1e-11 * max(np.max(np.abs(want)), 1e-300)
+        fro = float(np.vdot(g.ravel(), g.ravel()).real)
+        par = float(d * np.vdot(out, out).real)
+        assert abs(fro - par) <= 1e-10 * fro
+
+    check()
