@@ -112,6 +112,7 @@ struct K2Params {
     RunOut runs;
     OutMap map;                // MAPPED form
     double scale;
+    unsigned sb_ctas;          // K2s-c: CTAs per ZLO phase per X-mask superblock (0: one block)
 };
 
 // SEG = false: the whole walk from zero to coefficients (c_begin = 0, no partial sums); kept

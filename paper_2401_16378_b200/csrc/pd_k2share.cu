@@ -237,6 +237,9 @@ cudaError_t launch_gray_share(const K2Params& P0, bool seg, unsigned grid, size_
         P.c_end = P0.c_end << (P0.ci_log - cs_log);
         const uint64_t xblocks = (P0.x_count + (1ull << P.xc_log) - 1) >> P.xc_log;
         const uint64_t cgrid = xblocks << P.cpx_log;
+        static const char* sb_env = std::getenv("PD_K2SC_SB");  // measurement override
+        const uint64_t sb = sb_env ? std::strtoull(sb_env, nullptr, 10) : 0;
+        P.sb_ctas = (sb && sb < (cgrid >> 4)) ? static_cast<unsigned>(sb) : 0u;
         if (cgrid > 0x7fffffffull) return cudaErrorInvalidConfiguration;
         return seg ? launch_gray_share_c_seg(P, static_cast<unsigned>(cgrid), stream)
                    : launch_gray_share_c_full(P, static_cast<unsigned>(cgrid), stream);

@@ -268,8 +268,23 @@ __global__ void __launch_bounds__(kCThreads, 2) gray_share_c_kernel(const K2Para
     // blockIdx = ZLO * (grid / 16) + (xblock << (cpx_log - 4)) + zmid
     const unsigned mid_log = P.cpx_log - 4;
     const uint64_t per_zlo = gridDim.x >> 4;
-    const unsigned zlo = static_cast<unsigned>(blockIdx.x / per_zlo);
-    const uint64_t rest = blockIdx.x - zlo * per_zlo;
+    unsigned zlo;
+    uint64_t rest;
+    if (P.sb_ctas) {
+        // X-mask superblocks of sb_ctas CTAs per ZLO phase: all 16 phases of a superblock run
+        // before the next superblock starts, so its diagonals are re-read from L2 (the last
+        // superblock holds the remainder)
+        const uint64_t per_sb = 16ull * P.sb_ctas;
+        const uint64_t nfull = per_zlo / P.sb_ctas;
+        const uint64_t sbi = blockIdx.x / per_sb;
+        const uint64_t width = sbi < nfull ? P.sb_ctas : per_zlo - nfull * P.sb_ctas;
+        const uint64_t r = blockIdx.x - sbi * per_sb;
+        zlo = static_cast<unsigned>(r / width);
+        rest = sbi * P.sb_ctas + (r - static_cast<uint64_t>(zlo) * width);
+    } else {
+        zlo = static_cast<unsigned>(blockIdx.x / per_zlo);
+        rest = blockIdx.x - zlo * per_zlo;
+    }
     const uint64_t xblock = rest >> mid_log;
     const uint64_t zmid = rest & ((1ull << mid_log) - 1);
     CtaC t;
