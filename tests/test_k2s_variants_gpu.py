@@ -72,3 +72,10 @@ def test_host_pipeline_segments_bitwise(cuda, nq, kind):
     assert u[0] == w[0]
     if nq <= 13:
         assert u[0] == run(nq, kind, "host", {"PD_K2Q": "0"})[0]
+
+
+@pytest.mark.parametrize("nq,kind,sb", [(13, "normal", "40"), (14, "normal", "64"), (14, "band", "80")])
+def test_k2s_c_superblock_order_bitwise(cuda, nq, kind, sb):
+    """PD_K2SC_SB: the traffic-lean X-mask superblock order of K2s-c (a partial last superblock
+    at S = 40 and 80) computes every coefficient in the same order, so the bits are the same"""
+    assert run(nq, kind, "device", {"PD_K2SC_SB": sb})[0] == run(nq, kind, "device", {})[0]
