@@ -609,11 +609,19 @@ struct HostTimeline {
 
 // the pinned slot rings of pd_stage.h, created on the first pageable call (PD_STAGE_SLOT_MB,
 // PD_STAGE_WORKERS override the slot size and the worker count)
-int stager_of(pd_ctx* ctx, pdb::Stager** out) {
+// Slots are sized to the transfer (1/16 of it, 1 – 32 MiB), so a context that only ever moves
+// small matrices does not pin 640 MiB; a larger call replaces the rings once.
+int stager_of(pd_ctx* ctx, size_t bytes, pdb::Stager** out) {
+    const char* mb = std::getenv("PD_STAGE_SLOT_MB");
+    size_t slot = mb ? static_cast<size_t>(std::max(1, std::atoi(mb))) << 20 : size_t{32} << 20;
+    while (!mb && slot > (size_t{1} << 20) && slot * 16 > bytes) slot >>= 1;
+    if (ctx->stager && ctx->stager->slot_bytes() < slot) {
+        ctx->stager->finish();
+        delete ctx->stager;
+        ctx->stager = nullptr;
+    }
     if (!ctx->stager) {
-        const char* mb = std::getenv("PD_STAGE_SLOT_MB");
         const char* wk = std::getenv("PD_STAGE_WORKERS");
-        const size_t slot = (mb ? std::max(1, std::atoi(mb)) : 32) * (size_t{1} << 20);
         const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
         const unsigned workers = wk ? static_cast<unsigned>(std::atoi(wk)) : std::min(12u, hw - 2);
         ctx->stager = new pdb::Stager(ctx->device, slot, 4, 16, workers);
@@ -633,10 +641,12 @@ struct HostXfer {
     pdb::Stager* st = nullptr;
     bool up_staged = false, down_staged = false;
 
-    int init(pd_ctx* ctx, const void* g, const void* out) {
-        up_staged = g && pdb::host_pageable(g);
-        down_staged = out && pdb::host_pageable(out);
-        if (up_staged || down_staged) return stager_of(ctx, &st);
+    // transfers below kStageMin stay with the driver's own pageable copies (a few MiB at most)
+    static constexpr size_t kStageMin = size_t{8} << 20;
+    int init(pd_ctx* ctx, const void* g, const void* out, size_t bytes) {
+        up_staged = g && bytes >= kStageMin && pdb::host_pageable(g);
+        down_staged = out && bytes >= kStageMin && pdb::host_pageable(out);
+        if (up_staged || down_staged) return stager_of(ctx, bytes, &st);
         return PD_OK;
     }
     int up2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height,
@@ -683,7 +693,7 @@ struct HostXfer {
 int decompose_host(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_path path) {
     const size_t bytes = elems(N) * sizeof(double2);
     HostXfer xf;
-    if (int rc = xf.init(ctx, g, out)) return rc;
+    if (int rc = xf.init(ctx, g, out, bytes)) return rc;
     if (int rc = ctx->ensure(&ctx->g, &ctx->g_bytes, bytes)) return rc;
     if (int rc = ctx->ensure(&ctx->out, &ctx->out_bytes, bytes)) return rc;
     const uint64_t sb = pd_scratch_bytes(N, 1ull << N, path);

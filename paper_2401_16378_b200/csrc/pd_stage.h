@@ -54,6 +54,7 @@ public:
     Stager(int device, size_t slot_bytes, unsigned up_slots, unsigned down_slots, unsigned workers);
     ~Stager();
     bool ok() const { return ok_; }
+    size_t slot_bytes() const { return slot_bytes_; }
 
     // H2D of a height x width-byte rectangle (row pitches spitch on the host, dpitch on the
     // device) from pageable host memory, enqueued on `stream` in row bands
