@@ -611,7 +611,7 @@ struct HostTimeline {
 // PD_STAGE_WORKERS override the slot size and the worker count)
 // Slots are sized to the transfer (1/16 of it, 1 – 32 MiB), so a context that only ever moves
 // small matrices does not pin 640 MiB; a larger call replaces the rings once.
-int stager_of(pd_ctx* ctx, size_t bytes, pdb::Stager** out) {
+int stager_of(pd_ctx* ctx, size_t bytes, pdb::Stager** out, unsigned max_workers = 12) {
     const char* mb = std::getenv("PD_STAGE_SLOT_MB");
     size_t slot = mb ? static_cast<size_t>(std::max(1, std::atoi(mb))) << 20 : size_t{32} << 20;
     while (!mb && slot > (size_t{1} << 20) && slot * 16 > bytes) slot >>= 1;
@@ -623,7 +623,7 @@ int stager_of(pd_ctx* ctx, size_t bytes, pdb::Stager** out) {
     if (!ctx->stager) {
         const char* wk = std::getenv("PD_STAGE_WORKERS");
         const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
-        const unsigned workers = wk ? static_cast<unsigned>(std::atoi(wk)) : std::min(12u, hw - 2);
+        const unsigned workers = wk ? static_cast<unsigned>(std::atoi(wk)) : std::min(max_workers, hw - 2);
         ctx->stager = new pdb::Stager(ctx->device, slot, 4, 16, workers);
         if (!ctx->stager->ok()) {
             delete ctx->stager;
@@ -643,10 +643,10 @@ struct HostXfer {
 
     // transfers below kStageMin stay with the driver's own pageable copies (a few MiB at most)
     static constexpr size_t kStageMin = size_t{8} << 20;
-    int init(pd_ctx* ctx, const void* g, const void* out, size_t bytes) {
+    int init(pd_ctx* ctx, const void* g, const void* out, size_t bytes, unsigned max_workers = 12) {
         up_staged = g && bytes >= kStageMin && pdb::host_pageable(g);
         down_staged = out && bytes >= kStageMin && pdb::host_pageable(out);
-        if (up_staged || down_staged) return stager_of(ctx, bytes, &st);
+        if (up_staged || down_staged) return stager_of(ctx, bytes, &st, max_workers);
         return PD_OK;
     }
     int up2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height,
@@ -989,9 +989,17 @@ int decompose_multi(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pa
         return fail(PD_EINVAL, "multi-device decompositions run the GRAY or WHT path");
     const uint64_t B = dim >> p;                       // tile edge = X-masks per device
     const uint64_t run_len = 1ull << (2 * (N - p));
+    // pageable host buffers go through each device's own slot rings, the workers split
+    std::vector<HostXfer> xf(P);
+    const unsigned q = (B >= 512) ? 2u : (B >= 256 ? 1u : 0u);
+    const uint64_t Q = 1ull << q, Bs = B >> q;
+    const uint64_t piece = 1ull << (2 * (N - p - q));
     for (uint64_t d = 0; d < P; ++d) {
         pd_ctx* s = ctx->subs[d];
         if (int rc = bind(s)) return rc;
+        if (int rc = xf[d].init(s, g, out, (elems(N) >> p) * sizeof(double2),
+                                std::max<unsigned>(2, 12 / static_cast<unsigned>(P))))
+            return rc;
         const size_t gbytes = elems(N) * sizeof(double2);
         if (int rc = s->ensure(&s->g, &s->g_bytes, gbytes)) return rc;
         if (int rc = s->ensure(&s->out, &s->out_bytes, (elems(N) >> p) * sizeof(double2))) return rc;
@@ -1000,34 +1008,44 @@ int decompose_multi(pd_ctx* ctx, unsigned N, const double* g, double* out, pd_pa
         double* gd = static_cast<double*>(s->g);
         for (uint64_t t = 0; t < P; ++t) {
             const uint64_t off = 2 * (((t ^ d) * B) * dim + t * B);  // tile (t ^ d, t), in doubles
-            PD_CUDA(cudaMemcpy2DAsync(gd + off, dim * sizeof(double2), g + off, dim * sizeof(double2),
-                                      B * sizeof(double2), B, cudaMemcpyHostToDevice, s->stream));
+            if (int rc = xf[d].up2d(gd + off, dim * sizeof(double2), g + off, dim * sizeof(double2),
+                                    B * sizeof(double2), B, s->stream))
+                return rc;
         }
         // Q sub-blocks of the device's X-masks, each downloaded while the next computes. A
         // sub-block writes into the device's packed runs (rb = p, the fast run-pointer K2); its
         // coefficients there are P Q contiguous pieces of 4^(N-p-q): z's top p bits r select the
         // run, the next q digits (from x bits s and z bits u) the piece.
-        const unsigned q = (B >= 512) ? 2u : (B >= 256 ? 1u : 0u);
-        const uint64_t Q = 1ull << q, Bs = B >> q;
-        const uint64_t piece = 1ull << (2 * (N - p - q));
         double* so = static_cast<double*>(s->out);
         for (uint64_t sb_i = 0; sb_i < Q; ++sb_i) {
             if (int rc = pd_shard_coeffs_device(N, gd, d * B + sb_i * Bs, Bs, p, so, PD_LAYOUT_RUNS,
                                                 s->scratch, path, s->stream))
                 return rc;
             PD_CUDA(cudaEventRecord(s->block_done[sb_i], s->stream));
-            PD_CUDA(cudaStreamWaitEvent(s->d2h, s->block_done[sb_i], 0));
+        }
+    }
+    // every device's work is queued before any download: a pageable out can hold this thread
+    // until a staging slot drains
+    std::vector<pdb::Stager::Piece> pieces;
+    for (uint64_t d = 0; d < P; ++d) {
+        pd_ctx* s = ctx->subs[d];
+        if (int rc = bind(s)) return rc;
+        double* so = static_cast<double*>(s->out);
+        for (uint64_t sb_i = 0; sb_i < Q; ++sb_i) {
+            pieces.clear();
             for (uint64_t r = 0; r < P; ++r)
                 for (uint64_t u = 0; u < Q; ++u) {
                     const uint64_t host_off = pd_run_offset(N, p + q, d * Q + sb_i, r * Q + u);
                     const uint64_t dev_off = r * run_len + (pd_run_offset(q, q, sb_i, u) << (2 * (N - p - q)));
-                    PD_CUDA(cudaMemcpyAsync(out + 2 * host_off, so + 2 * dev_off, piece * sizeof(double2),
-                                            cudaMemcpyDeviceToHost, s->d2h));
+                    pieces.push_back({out + 2 * host_off, so + 2 * dev_off, piece * sizeof(double2)});
                 }
+            if (int rc = xf[d].down_pieces(pieces, s->block_done[sb_i], s->d2h)) return rc;
         }
     }
-    for (pd_ctx* s : ctx->subs) {
+    for (uint64_t d = 0; d < P; ++d) {
+        pd_ctx* s = ctx->subs[d];
         if (int rc = bind(s)) return rc;
+        if (int rc = xf[d].finish()) return rc;
         PD_CUDA(cudaStreamSynchronize(s->d2h));
         PD_CUDA(cudaStreamSynchronize(s->stream));
     }
