@@ -21,6 +21,7 @@ namespace {
 
 // pd_status -> the reference's exception types (decompose.cpp:14-19, matrix.cpp:10-19)
 void raise(int rc) {
+    if (rc == PD_OK) return;  // no message string on the success path (fixed memory)
     const std::string msg = pd_last_error();
     switch (rc) {
         case PD_OK: return;
