@@ -197,6 +197,30 @@ def n12_cpu_baseline(g, gpu_out):
             "matches_gpu_full_array": bool(np.array_equal(c, gpu_out))}
 
 
+def small_cpu_baseline(g, gpu_out, ns=None, reps=3):
+    """BASELINE configs[0-2] on the host, the reference's own code on every hardware thread:
+    decompose_parallel (full decompositions) or coeff_fast over a string batch (contiguous split),
+    best of `reps` wall-clock runs; its output must equal the GPU's bit for bit."""
+    import numpy as np
+    from oracle import oracle as O
+    ref = O.reference()
+    if ref is None:
+        return {"unavailable": "oracle/_ref not built"}
+    h = ref.matrix(g)
+    best, c = None, None
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        c = ref.decompose(h, threads=ref.cores) if ns is None else ref.coeff_batch(h, ns, threads=ref.cores)
+        sec = time.perf_counter() - t0
+        best = sec if best is None else min(best, sec)
+    return {"value": c.size / best, "unit": UNIT if ns is None else "strings/s", "cores": ref.cores,
+            "kind": "reference", "seconds": best,
+            "sample": ("full decomposition via reference decompose_parallel" if ns is None
+                       else f"{ns.size} strings via reference coeff_fast") + " (proj/src, -O3), best of "
+                      + str(reps),
+            "matches_gpu": bool(np.array_equal(c, gpu_out))}
+
+
 def run_reference_arm(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -534,6 +558,9 @@ def side_configs(pd, dev, stream, sptr, peaks, cpu_n12=True):
     res["n10_strings"] = {"config": "BASELINE configs[1]: 65,536 random strings of an N=10 matrix",
                           "value": 65536 / (ms / 1e3), "unit": "strings/s", "ms_per_step": ms,
                           "kernel": "K3b: bucketed by X-mask, one CTA per bucket over its staged diagonal"}
+    if cpu_n12:
+        res["n10_strings"]["cpu_baseline"] = small_cpu_baseline(
+            g.cpu().numpy(), o.cpu().numpy(), ns=ns.cpu().numpy().astype(np.uint64))
     # configs[2]: full N=10 decomposition of a Hermitian matrix (imaginary parts ~0)
     a = gen.standard_normal((2**nq, 2**nq)) + 1j * gen.standard_normal((2**nq, 2**nq))
     h = torch.from_numpy((a + a.conj().T) / 2).to(dev)
@@ -543,6 +570,8 @@ def side_configs(pd, dev, stream, sptr, peaks, cpu_n12=True):
     res["n10_hermitian_full"] = {"config": "BASELINE configs[2]: full N=10 decomposition of (A+A^H)/2",
                                  "value": 4**nq / (ms / 1e3), "unit": UNIT, "ms_per_step": ms,
                                  "max_abs_imag": float(torch.max(torch.abs(out.imag)))}
+    if cpu_n12:
+        res["n10_hermitian_full"]["cpu_baseline"] = small_cpu_baseline(h.cpu().numpy(), out.cpu().numpy())
     # configs[0]: full N=6 decomposition (latency of one small call on the device)
     nq = 6
     g6 = torch.from_numpy(gen.standard_normal((64, 64)) + 1j * gen.standard_normal((64, 64))).to(dev)
@@ -551,6 +580,8 @@ def side_configs(pd, dev, stream, sptr, peaks, cpu_n12=True):
     ms = ev_time(lambda: pd.device.decompose(nq, g6.data_ptr(), o6.data_ptr(), s6.data_ptr(), "gray", sptr), 50)
     res["n6_full"] = {"config": "BASELINE configs[0]: full N=6 decomposition", "value": 4**nq / (ms / 1e3),
                       "unit": UNIT, "ms_per_step": ms}
+    if cpu_n12:
+        res["n6_full"]["cpu_baseline"] = small_cpu_baseline(g6.cpu().numpy(), o6.cpu().numpy(), reps=20)
     return res
 
 
