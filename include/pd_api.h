@@ -88,7 +88,12 @@ PD_EXPORT void* pd_ctx_stream(pd_ctx* ctx);
 /* All 4^N coefficients of the 2^N x 2^N matrix g, written to out (2*4^N doubles).
  * Replaces decompose_parallel(const DenseMatrix&, unsigned threads)
  * (decompose.hpp:46, decompose.cpp:95-131,205-207) and
- * decompose_serial_quaternary (decompose.hpp:55; same output). */
+ * decompose_serial_quaternary (decompose.hpp:55; same output).
+ * g and out may be page-locked (cudaHostAlloc / cudaHostRegister: copied by DMA directly) or
+ * ordinary pageable memory (copied through the context's pinned staging slots on host worker
+ * threads; env PD_STAGE_WORKERS, PD_STAGE_SLOT_MB), decided per buffer. On any error the call
+ * returns only after all of its queued copies and kernels have finished, so the caller may
+ * free g and out at once. */
 PD_EXPORT int pd_decompose(pd_ctx* ctx, unsigned num_qubits, const double* g, double* out, pd_path path);
 
 /* One coefficient c_n, written to out[0..1].
