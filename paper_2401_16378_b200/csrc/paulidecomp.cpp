@@ -88,11 +88,47 @@ std::uint64_t fast_mults(unsigned N) { return N + 2 * (std::uint64_t{1} << N) - 
 
 }  // namespace
 
+namespace {
+
+// The reference API returns its coefficients (and matrices) by value in value-initialised
+// std::vectors. Its
+// zero fill first-touches 4 GiB at N=14 on one thread (~1.3 s of page faults and zeroing, four
+// times the GPU call); the pages are populated on helper threads first (MADV_HUGEPAGE where the
+// box runs THP in madvise mode, then MADV_POPULATE_WRITE: allocated and zeroed by the kernel),
+// so the fill that follows runs over resident pages.
+std::vector<Complex> result_vector(std::uint64_t n) {
+    std::vector<Complex> v;
+    const std::uint64_t bytes = n * sizeof(Complex);
+    if (bytes >= (std::uint64_t{64} << 20)) {
+        v.reserve(n);
+        const uintptr_t page = 4096, huge = uintptr_t{2} << 20;
+        const uintptr_t lo = reinterpret_cast<uintptr_t>(v.data()), hi = lo + bytes;
+        const uintptr_t hlo = (lo + huge - 1) & ~(huge - 1), hhi = hi & ~(huge - 1);
+        if (hhi > hlo) madvise(reinterpret_cast<void*>(hlo), hhi - hlo, MADV_HUGEPAGE);
+#ifdef MADV_POPULATE_WRITE
+        const uintptr_t b = (lo + page - 1) & ~(page - 1), e = hi & ~(page - 1);
+        std::atomic<uintptr_t> next{b};
+        std::vector<std::thread> pool;
+        for (int k = 0; k < 8; ++k)
+            pool.emplace_back([&] {
+                constexpr uintptr_t kPiece = uintptr_t{32} << 20;
+                for (uintptr_t at; (at = next.fetch_add(kPiece)) < e;)
+                    if (madvise(reinterpret_cast<void*>(at), std::min(kPiece, e - at), MADV_POPULATE_WRITE)) return;
+            });
+        for (auto& t : pool) t.join();
+#endif
+    }
+    v.resize(n);
+    return v;
+}
+
+}  // namespace
+
 // ---------------- DenseMatrix (matrix.hpp:14-43 semantics) ----------------
 
 DenseMatrix::DenseMatrix(unsigned num_qubits) : num_qubits_(num_qubits) {
     check_qubit_count(num_qubits);
-    elements_.assign(std::uint64_t{1} << (2 * num_qubits), Complex{0.0, 0.0});
+    elements_ = result_vector(std::uint64_t{1} << (2 * num_qubits));
 }
 
 DenseMatrix::DenseMatrix(unsigned num_qubits, std::vector<Complex> elements)
@@ -221,41 +257,6 @@ DenseMatrix random_matrix(unsigned num_qubits, std::uint64_t seed) {  // bench.c
     raise(pd_random_matrix(l.ctx, num_qubits, seed, as_doubles(m.data())));
     return m;
 }
-
-namespace {
-
-// The reference API returns its coefficients by value in a value-initialised std::vector. Its
-// zero fill first-touches 4 GiB at N=14 on one thread (~1.3 s of page faults and zeroing, four
-// times the GPU call); the pages are populated on helper threads first (MADV_HUGEPAGE where the
-// box runs THP in madvise mode, then MADV_POPULATE_WRITE: allocated and zeroed by the kernel),
-// so the fill that follows runs over resident pages.
-std::vector<Complex> result_vector(std::uint64_t n) {
-    std::vector<Complex> v;
-    const std::uint64_t bytes = n * sizeof(Complex);
-    if (bytes >= (std::uint64_t{64} << 20)) {
-        v.reserve(n);
-        const uintptr_t page = 4096, huge = uintptr_t{2} << 20;
-        const uintptr_t lo = reinterpret_cast<uintptr_t>(v.data()), hi = lo + bytes;
-        const uintptr_t hlo = (lo + huge - 1) & ~(huge - 1), hhi = hi & ~(huge - 1);
-        if (hhi > hlo) madvise(reinterpret_cast<void*>(hlo), hhi - hlo, MADV_HUGEPAGE);
-#ifdef MADV_POPULATE_WRITE
-        const uintptr_t b = (lo + page - 1) & ~(page - 1), e = hi & ~(page - 1);
-        std::atomic<uintptr_t> next{b};
-        std::vector<std::thread> pool;
-        for (int k = 0; k < 8; ++k)
-            pool.emplace_back([&] {
-                constexpr uintptr_t kPiece = uintptr_t{32} << 20;
-                for (uintptr_t at; (at = next.fetch_add(kPiece)) < e;)
-                    if (madvise(reinterpret_cast<void*>(at), std::min(kPiece, e - at), MADV_POPULATE_WRITE)) return;
-            });
-        for (auto& t : pool) t.join();
-#endif
-    }
-    v.resize(n);
-    return v;
-}
-
-}  // namespace
 
 PauliDecomposition decompose(const DenseMatrix& g, Path path) {
     PauliDecomposition d{g.num_qubits(), result_vector(g.element_count())};
