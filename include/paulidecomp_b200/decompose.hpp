@@ -121,6 +121,10 @@ void decompose_into(const Complex* g, unsigned num_qubits, Complex* out, Path pa
                     const std::vector<int>& devices);
 PauliDecomposition decompose(const DenseMatrix& g, Path path = Path::Gray);
 
+// the matrix of the 4^N coefficients at c into g_out (2^N x 2^N, row-major): recompose without
+// the by-value containers
+void recompose_into(const Complex* c, unsigned num_qubits, Complex* g_out);
+
 // out[k] = c_{ns[k]}
 void coeff_batch_into(const Complex* g, unsigned num_qubits, const std::uint64_t* ns,
                       std::uint64_t count, Complex* out);

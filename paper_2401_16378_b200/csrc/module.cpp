@@ -157,14 +157,20 @@ py::array_t<Complex> py_recompose(const ComplexArray& c) {  // module.cpp:45-54 
     if (count < 4 || !std::has_single_bit(count) || (std::countr_zero(count) & 1))
         throw std::invalid_argument("coefficient count must be a power of four >= 4");
     const unsigned N = static_cast<unsigned>(std::countr_zero(count) / 2);
-    PauliDecomposition d{N, std::vector<Complex>(c.data(), c.data() + count)};
-    DenseMatrix m(1);
+    if (N >= kMaxQubits) throw std::length_error("a dense matrix for N=32 exceeds the address space");
+    // the coefficients are read in place and the matrix is written straight into the returned
+    // array (the reference binding copies both ways, module.cpp:45-54)
+    py::array_t<Complex> result = new_result(static_cast<py::ssize_t>(count));
+    const Complex* src = c.data();
+    Complex* dst = result.mutable_data();
     {
         py::gil_scoped_release nogil;
-        m = recompose(d);
+        std::unique_ptr<Prefault> prefault;
+        if (count * sizeof(Complex) >= (size_t{64} << 20)) prefault = std::make_unique<Prefault>(dst, count * sizeof(Complex), 2);
+        recompose_into(src, N, dst);
     }
-    const auto dim = static_cast<py::ssize_t>(m.dim());
-    return py::array_t<Complex>({dim, dim}, m.data());
+    const auto dim = static_cast<py::ssize_t>(std::uint64_t{1} << N);
+    return result.reshape({dim, dim});
 }
 
 Complex py_coefficient_index(const ComplexArray& g, std::uint64_t n, bool slow) {

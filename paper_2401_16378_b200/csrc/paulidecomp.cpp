@@ -293,6 +293,12 @@ std::vector<Complex> coeff_batch(const DenseMatrix& g, const std::vector<std::ui
     return out;
 }
 
+void recompose_into(const Complex* c, unsigned num_qubits, Complex* g_out) {
+    check_qubit_count(num_qubits);
+    Lease l = lease();
+    raise(pd_recompose(l.ctx, num_qubits, as_doubles(c), as_doubles(g_out)));
+}
+
 DenseMatrix recompose(const PauliDecomposition& d) {  // decompose.cpp:221-230 validation
     if (d.num_qubits == 0 || d.num_qubits > kMaxQubits)
         throw std::invalid_argument("qubit count must be in [1, 32]");

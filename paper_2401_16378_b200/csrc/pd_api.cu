@@ -1066,21 +1066,31 @@ int pd_random_matrix(pd_ctx* ctx, unsigned N, uint64_t seed, double* g_out) {
     return PD_OK;
 }
 
-int pd_recompose(pd_ctx* ctx, unsigned N, const double* coeffs, double* g_out) {
-    if (int rc = check_qubits(N)) return rc;
-    if (int rc = bind(ctx)) return rc;
-    if (!coeffs || !g_out) return fail(PD_EINVAL, "null buffer");
+namespace {
+// host buffers of either kind (HostXfer: pinned by DMA, pageable through the staging slots)
+int recompose_host(pd_ctx* ctx, unsigned N, const double* coeffs, double* g_out) {
     const size_t bytes = elems(N) * sizeof(double2);
     if (int rc = ctx->ensure(&ctx->g, &ctx->g_bytes, bytes)) return rc;
     if (int rc = ctx->ensure(&ctx->out, &ctx->out_bytes, bytes)) return rc;
     if (int rc = ctx->ensure(&ctx->scratch, &ctx->scratch_bytes, bytes)) return rc;
-    if (int rc = upload(ctx, ctx->out, coeffs, bytes)) return rc;
+    HostXfer xf;
+    if (int rc = xf.init(ctx, coeffs, g_out, bytes)) return rc;
+    if (int rc = xf.up(ctx->out, coeffs, bytes, ctx->stream)) return rc;
     if (int rc = pd_recompose_device(N, static_cast<const double*>(ctx->out),
                                      static_cast<double*>(ctx->g), ctx->scratch, ctx->stream))
         return rc;
-    PD_CUDA(cudaMemcpyAsync(g_out, ctx->g, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    if (int rc = xf.down(g_out, ctx->g, bytes, nullptr, ctx->stream)) return rc;
+    if (int rc = xf.finish()) return rc;
     PD_CUDA(cudaStreamSynchronize(ctx->stream));
     return PD_OK;
+}
+}  // namespace
+
+int pd_recompose(pd_ctx* ctx, unsigned N, const double* coeffs, double* g_out) {
+    if (int rc = check_qubits(N)) return rc;
+    if (int rc = bind(ctx)) return rc;
+    if (!coeffs || !g_out) return fail(PD_EINVAL, "null buffer");
+    return drained(ctx, recompose_host(ctx, N, coeffs, g_out));
 }
 
 int pd_coeff_batch(pd_ctx* ctx, unsigned N, const double* g, const uint64_t* ns, uint64_t count,
