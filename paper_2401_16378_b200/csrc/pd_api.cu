@@ -1061,7 +1061,11 @@ int pd_random_matrix(pd_ctx* ctx, unsigned N, uint64_t seed, double* g_out) {
     const size_t bytes = elems(N) * sizeof(double2);
     if (int rc = ctx->ensure(&ctx->g, &ctx->g_bytes, bytes)) return rc;
     if (int rc = pd_random_matrix_device(N, seed, static_cast<double*>(ctx->g), ctx->stream)) return rc;
-    PD_CUDA(cudaMemcpyAsync(g_out, ctx->g, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    HostXfer xf;  // to host memory of either kind (pageable: the staging slots)
+    int rc = xf.init(ctx, nullptr, g_out, bytes);
+    if (rc == PD_OK) rc = xf.down(g_out, ctx->g, bytes, nullptr, ctx->stream);
+    if (rc == PD_OK) rc = xf.finish();
+    if (rc != PD_OK) return drained(ctx, rc);
     PD_CUDA(cudaStreamSynchronize(ctx->stream));
     return PD_OK;
 }
@@ -1093,6 +1097,11 @@ int pd_recompose(pd_ctx* ctx, unsigned N, const double* coeffs, double* g_out) {
     return drained(ctx, recompose_host(ctx, N, coeffs, g_out));
 }
 
+namespace {
+int coeff_batch_host(pd_ctx* ctx, unsigned N, const double* g, const uint64_t* ns, uint64_t count,
+                     double* out);
+}
+
 int pd_coeff_batch(pd_ctx* ctx, unsigned N, const double* g, const uint64_t* ns, uint64_t count,
                    double* out) {
     if (int rc = check_qubits(N)) return rc;
@@ -1101,6 +1110,12 @@ int pd_coeff_batch(pd_ctx* ctx, unsigned N, const double* g, const uint64_t* ns,
         if (int rc = check_index(N, ns[k])) return rc;
     if (int rc = bind(ctx)) return rc;
     if (count == 0) return PD_OK;
+    return drained(ctx, coeff_batch_host(ctx, N, g, ns, count, out));
+}
+
+namespace {
+int coeff_batch_host(pd_ctx* ctx, unsigned N, const double* g, const uint64_t* ns, uint64_t count,
+                     double* out) {
     const size_t gbytes = elems(N) * sizeof(double2);
     const uint64_t dim = 1ull << N;
     // few X-masks among the strings (at most 2^N / 8): upload only their gathered diagonals
@@ -1149,7 +1164,9 @@ int pd_coeff_batch(pd_ctx* ctx, unsigned N, const double* g, const uint64_t* ns,
     if (int rc = ctx->ensure(&ctx->g, &ctx->g_bytes, gbytes)) return rc;
     if (int rc = ctx->ensure(&ctx->ns, &ctx->ns_bytes, count * sizeof(uint64_t))) return rc;
     if (int rc = ctx->ensure(&ctx->out, &ctx->out_bytes, count * sizeof(double2))) return rc;
-    if (int rc = upload(ctx, ctx->g, g, gbytes)) return rc;
+    HostXfer xf;  // the matrix from host memory of either kind (pageable: the staging slots)
+    if (int rc = xf.init(ctx, g, nullptr, gbytes)) return rc;
+    if (int rc = xf.up(ctx->g, g, gbytes, ctx->stream)) return rc;
     if (int rc = upload(ctx, ctx->ns, ns, count * sizeof(uint64_t))) return rc;
     if (int rc = pd_coeff_batch_device(N, static_cast<const double*>(ctx->g),
                                        static_cast<const uint64_t*>(ctx->ns), count, 0,
@@ -1160,6 +1177,7 @@ int pd_coeff_batch(pd_ctx* ctx, unsigned N, const double* g, const uint64_t* ns,
     PD_CUDA(cudaStreamSynchronize(ctx->stream));
     return PD_OK;
 }
+}  // namespace
 
 int pd_coeff(pd_ctx* ctx, unsigned N, const double* g, uint64_t n, int slow, double* out) {
     if (int rc = check_qubits(N)) return rc;
