@@ -14,5 +14,7 @@ std::uint64_t matrix_seed(std::uint64_t seed, unsigned num_qubits, unsigned rep)
 // bench.cpp:48-58: uniform [-1, 1) real and imaginary parts from splitmix64, generated on the
 // device (K5, bit-identical) and copied back
 DenseMatrix random_matrix(unsigned num_qubits, std::uint64_t seed);
+// B200 addition: the same matrix into caller-owned memory (4^N entries)
+void random_matrix_into(unsigned num_qubits, std::uint64_t seed, Complex* out);
 
 }  // namespace paulidecomp

@@ -47,6 +47,7 @@ unsigned matrix_qubits(const ComplexArray& a) {
 // cost more than the whole decomposition (N=14: 605 ms per call against 370 ms into an array
 // that was already touched).
 py::array_t<Complex> new_result(py::ssize_t count) {
+    if (count < 0 || static_cast<size_t>(count) > (size_t{1} << 58)) throw std::bad_alloc();
     const size_t bytes = static_cast<size_t>(count) * sizeof(Complex);
     constexpr size_t kHuge = size_t{2} << 20;
     static const char* thp = std::getenv("PD_RESULT_THP");  // "0": a plain numpy array (A/B)
@@ -319,11 +320,21 @@ PYBIND11_MODULE(_paulidecomp, m) {
     m.def("matrix_seed", &matrix_seed, py::arg("seed"), py::arg("num_qubits"), py::arg("rep"),
           "The reference benchmark's per-(N, rep) generator seed (bench.cpp:42-46).");
     m.def("random_matrix", [](unsigned N, std::uint64_t seed) {
-        DenseMatrix g = random_matrix(N, seed);
-        const py::ssize_t dim = static_cast<py::ssize_t>(g.dim());
-        py::array_t<Complex> a({dim, dim});
-        std::memcpy(a.mutable_data(), g.data(), g.element_count() * sizeof(Complex));
-        return a;
+        if (N == 0 || N >= kMaxQubits) {
+            DenseMatrix probe(N);  // the reference's errors (matrix.cpp:10-19)
+        }
+        // generated on the device straight into the returned array (no DenseMatrix round trip)
+        const py::ssize_t count = static_cast<py::ssize_t>(1) << (2 * N);
+        py::array_t<Complex> a = new_result(count);
+        Complex* dst = a.mutable_data();
+        {
+            py::gil_scoped_release nogil;
+            std::unique_ptr<Prefault> prefault;
+            if (count * sizeof(Complex) >= (size_t{64} << 20)) prefault = std::make_unique<Prefault>(dst, count * sizeof(Complex), 2);
+            random_matrix_into(N, seed, dst);
+        }
+        const py::ssize_t dim = static_cast<py::ssize_t>(1) << N;
+        return a.reshape({dim, dim});
     }, py::arg("num_qubits"), py::arg("seed"),
           "random_matrix(N, seed) of the reference benchmark (bench.cpp:48-58), generated on the GPU.");
     py::module_ d = m.def_submodule("device", "Stream-ordered entry points on device pointers");

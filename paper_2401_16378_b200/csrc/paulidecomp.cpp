@@ -251,6 +251,12 @@ std::uint64_t matrix_seed(std::uint64_t seed, unsigned num_qubits, unsigned rep)
     return z ^ (z >> 31);
 }
 
+void random_matrix_into(unsigned num_qubits, std::uint64_t seed, Complex* out) {
+    check_qubit_count(num_qubits);
+    Lease l = lease();
+    raise(pd_random_matrix(l.ctx, num_qubits, seed, as_doubles(out)));
+}
+
 DenseMatrix random_matrix(unsigned num_qubits, std::uint64_t seed) {  // bench.cpp:48-58, on the GPU
     DenseMatrix m(num_qubits);
     Lease l = lease();
