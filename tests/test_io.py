@@ -246,3 +246,35 @@ def test_coefficient_reader_agrees_with_reference(pd, ref, tmp_path, k):
     p = str(tmp_path / "c.csv")
     open(p, "w", newline="").write(COEF_TEXTS[k])
     _same_outcome(lambda: pd.read_coefficients(p), lambda: ref.read_coefficients(p))
+
+
+@pytest.mark.gpu
+def test_cli_bench_csv_schema(pd, port, cuda, tmp_path):
+    """`pdb200 bench`: docs/formats.md's benchmark CSV — per (N, path) one row per repetition
+    (the matrix_seed of that repetition, an empty stddev field) and then the rep = -1 summary
+    (master seed, mean, sample stddev); paths fast / slow / serial-quaternary with the exact
+    multiplication counts of proj/README.md:115-120; only the timing fields vary between runs."""
+    import csv as csvmod
+    outs = []
+    for k in range(2):
+        out = str(tmp_path / f"b{k}.csv")
+        r = subprocess.run([CLI, "bench", "--n-min", "1", "--n-max", "4", "--reps", "3", "--seed", "11",
+                            "--out", out], capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr
+        outs.append(list(csvmod.reader(open(out))))
+    a, b = outs
+    assert a[0] == ["N", "path", "threads", "rep", "seed", "seconds", "mult_count", "seconds_stddev"]
+    assert len(a) == 1 + 4 * 3 * 4 and len(b) == len(a)
+    counts = {"fast": lambda n: 4**n * (n + 2 * 2**n - 1), "slow": lambda n: 4**n * (n + 1) * 2**n,
+              "serial-quaternary": lambda n: n + 4**n * (2 * 2**n - 1) + (4**n - 1)}
+    for ra, rb in zip(a[1:], b[1:]):
+        assert [ra[k] for k in (0, 1, 2, 3, 4, 6)] == [rb[k] for k in (0, 1, 2, 3, 4, 6)]
+        nq, path, rep, seed = int(ra[0]), ra[1], int(ra[3]), int(ra[4])
+        assert int(ra[6]) == counts[path](nq) and float(ra[5]) > 0
+        if rep >= 0:
+            assert seed == port.matrix_seed(11, nq, rep) and ra[7] == ""
+        else:
+            assert seed == 11 and float(ra[7]) >= 0
+    for args in (["bench", "--n-max", "9"], ["bench", "--reps", "0"], ["bench", "--n-min", "3", "--n-max", "2"],
+                 ["bench", "--seed", "-1"]):
+        assert subprocess.run([CLI, *args], capture_output=True, timeout=60).returncode == 1, args

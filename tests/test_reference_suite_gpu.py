@@ -3,10 +3,9 @@
 * proj/tests/python/test_smoke.py (9 tests) with `import paulidecomp` resolving to
   tests/reference_suite/paulidecomp, the reference package's re-export over this package.
 * proj/tests/acceptance.cpp, compiled unmodified against include/compat/paulidecomp/*.hpp and
-  linked with libpaulidecomp_b200.so (oracle/Makefile `suite`). Criteria 1-8 are the
-  library's guarantees and must PASS. Criterion 9 drives the reference CLI's `bench`
-  subcommand and its CSV, the benchmark harness SURVEY.md §2 marks out of scope; our pdb200
-  has no `bench`, so 9 is reported and must fail for exactly that reason.
+  linked with libpaulidecomp_b200.so (oracle/Makefile `suite`). All nine criteria must PASS:
+  1-8 are the library's guarantees, 9 drives the CLI (pdb200: decompose/recompose round trip,
+  exit codes, and the `bench` CSV of docs/formats.md, deterministic in all but its timings).
 
 Both files are copied from /root/reference at build time into the git-ignored oracle/_ref/suite
 (they travel to the GPU box with the snapshot; nothing reads /root/reference at run time)."""
@@ -53,7 +52,6 @@ def test_reference_acceptance_criteria(cuda):
     r = subprocess.run([exe, cli], capture_output=True, text=True, timeout=900)
     status = {int(m.group(2)): m.group(1) for m in re.finditer(r"^(PASS|FAIL) (\d+)/9 ", r.stdout, re.M)}
     assert sorted(status) == list(range(1, 10)), r.stdout
-    for k in range(1, 9):
+    for k in range(1, 10):
         assert status[k] == "PASS", r.stdout
-    # criterion 9 passes the CLI pipeline and exit-code checks and stops at `pdb200 bench`
-    assert status[9] == "FAIL" and "bench exited nonzero" in r.stdout, r.stdout
+    assert r.returncode == 0, r.stdout
