@@ -278,3 +278,23 @@ def test_cli_bench_csv_schema(pd, port, cuda, tmp_path):
     for args in (["bench", "--n-max", "9"], ["bench", "--reps", "0"], ["bench", "--n-min", "3", "--n-max", "2"],
                  ["bench", "--seed", "-1"]):
         assert subprocess.run([CLI, *args], capture_output=True, timeout=60).returncode == 1, args
+
+
+@pytest.mark.parametrize("nq,cells", [(4, [(5, 2)]), (10, [(1000, 7), (300, 1023), (900, 0)])])
+def test_binary_reader_reports_first_non_finite(pd, tmp_path, nq, cells):
+    # the binary reader fills the array in place and scans it on several threads (N=10: 2^20
+    # elements); the reported element is the first in row-major order, like the text reader's
+    g = normal_matrix(np.random.default_rng(nq), nq)
+    for r, c in cells:
+        g[r, c] = complex(0.0, np.inf) if r % 2 else complex(np.nan, 0.0)
+    p = str(tmp_path / "m.bin")
+    with open(p, "wb") as f:
+        f.write(b"PDMAT-V1" + nq.to_bytes(8, "little") + g.tobytes())
+    r, c = min(cells)
+    with pytest.raises(ValueError, match=f"row {r}, column {c}$"):
+        pd.read_matrix(p, "binary")
+    g2 = normal_matrix(np.random.default_rng(nq + 1), nq)
+    with open(p, "wb") as f:
+        f.write(b"PDMAT-V1" + nq.to_bytes(8, "little") + g2.tobytes())
+    back = pd.read_matrix(p, "binary")
+    assert back.shape == g2.shape and np.array_equal(back.view(np.uint64), g2.view(np.uint64))
