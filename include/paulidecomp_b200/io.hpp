@@ -31,6 +31,8 @@ std::string format_double(double value);
 // ---- matrices ----
 DenseMatrix read_matrix(const std::string& path, MatrixFormat format);
 void write_matrix(const DenseMatrix& matrix, const std::string& path, MatrixFormat format);
+// view form: the row-major 2^N x 2^N matrix at g (no DenseMatrix copy)
+void write_matrix_view(const Complex* g, unsigned num_qubits, const std::string& path, MatrixFormat format);
 DenseMatrix read_matrix_text(std::istream& in);
 DenseMatrix read_matrix_binary(std::istream& in);
 void write_matrix_text(const DenseMatrix& matrix, std::ostream& out);

@@ -333,8 +333,10 @@ PYBIND11_MODULE(_paulidecomp, m) {
     }, py::arg("path"), py::arg("format") = "text");
     m.def("write_matrix", [mfmt](const ComplexArray& a, const std::string& path, const std::string& format) {
         const unsigned N = matrix_qubits(a);
-        DenseMatrix g(N, std::vector<Complex>(a.data(), a.data() + a.size()));
-        write_matrix(g, path, mfmt(format));
+        const Complex* g = a.data();
+        const MatrixFormat f = mfmt(format);
+        py::gil_scoped_release nogil;
+        write_matrix_view(g, N, path, f);
     }, py::arg("matrix"), py::arg("path"), py::arg("format") = "text");
     m.def("read_coefficients", [](const std::string& path) {
         PauliDecomposition d = read_coefficients(path);
