@@ -460,25 +460,34 @@ __global__ void __launch_bounds__(kWhtThreads, 2)
     const uint64_t grp = blockIdx.x & ((1u << groups_log) - 1);   // r_hi: rows grp*128 ..
     const uint64_t xb = blockIdx.x >> groups_log;
     const uint64_t xh = (x0 >> 5) + xb;
-    // index bits 3-4 while loading 128 B lines of E' (and dropping them from L2)
+    // index bits 3-4 while loading 128 B lines of E' (and dropping them from L2): all 16 loads
+    // of the thread are issued before any is used, and a line is discarded only after its
+    // values have been consumed
+    double2 u[4][4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         const unsigned g = threadIdx.x + q * kWhtThreads, clo = g & 7, row = g >> 3;
         const unsigned x5 = row >> 2, rb = row & 3;
         const double2* src = eprime + ((xb << 5) + x5) * dim + (grp << kLoBits) + rb * 32 + clo;
-        double2 u[4];
 #pragma unroll
-        for (int h = 0; h < 4; ++h) u[h] = __ldcs(src + h * 8);
-        if (clo == 0)
+        for (int h = 0; h < 4; ++h) u[q][h] = __ldcs(src + h * 8);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const unsigned g = threadIdx.x + q * kWhtThreads, clo = g & 7, row = g >> 3;
+        const unsigned x5 = row >> 2, rb = row & 3;
+        bfly(u[q][0], u[q][1]);
+        bfly(u[q][2], u[q][3]);
+        bfly(u[q][0], u[q][2]);
+        bfly(u[q][1], u[q][3]);
+#pragma unroll
+        for (int h = 0; h < 4; ++h) sb[(rb * 32 + x5) * kP1bRow + h * 8 + clo] = u[q][h];
+        if (clo == 0) {
+            const double2* src = eprime + ((xb << 5) + x5) * dim + (grp << kLoBits) + rb * 32;
 #pragma unroll
             for (int h = 0; h < 4; ++h)
                 asm volatile("discard.global.L2 [%0], 128;" ::"l"(src + h * 8) : "memory");
-        bfly(u[0], u[1]);
-        bfly(u[2], u[3]);
-        bfly(u[0], u[2]);
-        bfly(u[1], u[3]);
-#pragma unroll
-        for (int h = 0; h < 4; ++h) sb[(rb * 32 + x5) * kP1bRow + h * 8 + clo] = u[h];
+        }
     }
     __syncthreads();
     // index bits 0-2
