@@ -453,6 +453,33 @@ def run_ours(args) -> None:
                                              "kernel": "K4 fused two-pass WHT", "k4_ms": k4w}}
             line["wht_path"]["roofline"]["frac"] = (line["wht_path"]["roofline"]["achieved"]
                                                     / line["wht_path"]["roofline"]["peak"])
+            # recompose (the inverse) of the last step's coefficients into a second
+            # matrix, checked against G: the chunked inverse WHT passes, HBM-bound at 32*4^N B
+            if world == 1 and args.path == "gray":
+                scr = diag if diag is not None else scratch_tensor(nq, plan.x_count, "wht", dev)
+                g2 = torch.empty_like(G)
+
+                def rec():
+                    pd.device.recompose(nq, out.data_ptr(), g2.data_ptr(), scr.data_ptr(), sptr)
+                for _ in range(3):
+                    rec()
+                torch.cuda.synchronize()
+                ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                ea.record(stream)
+                for _ in range(args.steps):
+                    rec()
+                eb.record(stream)
+                torch.cuda.synchronize()
+                rms = ea.elapsed_time(eb) / args.steps
+                err = float(torch.max(torch.abs(g2 - G)))
+                del g2
+                hbm = float(peaks.get("hbm_gbs", 6542.7))
+                line["recompose"] = {"ms_per_step": rms, "unit": "GB/s",
+                                     "roofline": {"bound": "hbm", "achieved": 32.0 * 4**nq / (rms / 1e3) / 1e9,
+                                                  "peak": hbm, "unit": "GB/s",
+                                                  "frac": 32.0 * 4**nq / (rms / 1e3) / 1e9 / hbm,
+                                                  "algorithmic": "32*4^N B (read coefficients, write G)"},
+                                     "max_abs_err_vs_G": err}
         if world == 1 and rank == 0:
             line["side_configs"] = side_configs(pd, dev, stream, sptr, peaks, not args.no_cpu_baseline)
 
